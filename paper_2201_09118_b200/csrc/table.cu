@@ -1,0 +1,233 @@
+// table.cu -- K1: canonical codebook and two-level decode tables on device.
+//
+// Canonical numbering restates codebook.py:86-112 (symbols sorted by (length,
+// symbol) get consecutive codes, shifting left on every length increase) and
+// the per-length first_code / first_index recurrence of codebook.py:209-233.
+// Instead of the reference's per-bit first_code loop (kernels.py:35-44) the
+// device decodes through:
+//   * lut  : 2^11-entry first-level table (symbol, length) in shared memory,
+//   * cnt  : 2^11-entry multi-codeword count table (codewords fully inside the
+//            11-bit window, bits they consume) for count-only passes,
+//   * lj   : left-justified codes in ascending order for long codes (binary
+//            search, exact for any prefix-free code -- see common.cuh).
+#include "common.cuh"
+
+namespace bh {
+
+__device__ __forceinline__ void table_ptrs(void* blob, uint32_t max_codes, TableHdr*& hdr,
+                                           uint32_t*& lut, uint16_t*& cnt, uint32_t*& lj,
+                                           uint16_t*& ljsym, uint8_t*& ljlen) {
+  TableLayout L(max_codes);
+  char* b = static_cast<char*>(blob);
+  hdr = reinterpret_cast<TableHdr*>(b);
+  lut = reinterpret_cast<uint32_t*>(b + L.lut);
+  cnt = reinterpret_cast<uint16_t*>(b + L.cnt);
+  lj = reinterpret_cast<uint32_t*>(b + L.lj);
+  ljsym = reinterpret_cast<uint16_t*>(b + L.ljsym);
+  ljlen = reinterpret_cast<uint8_t*>(b + L.ljlen);
+}
+
+// Single CTA (1024 threads): counting sort by (length, symbol), canonical codes.
+__global__ void __launch_bounds__(1024) k_canonical(const uint8_t* __restrict__ lengths,
+                                                    uint32_t alphabet, void* blob,
+                                                    uint32_t max_codes, uint32_t* codes_out) {
+  __shared__ uint32_t s_count[33];
+  __shared__ unsigned long long s_fc[33];
+  __shared__ uint32_t s_fi[33];
+  __shared__ uint32_t s_fill[33];
+  __shared__ uint32_t s_wcnt[32][33];
+  __shared__ int s_bad;
+  TableHdr* hdr; uint32_t* lut; uint16_t* cnt; uint32_t* lj; uint16_t* ljsym; uint8_t* ljlen;
+  table_ptrs(blob, max_codes, hdr, lut, cnt, lj, ljsym, ljlen);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid < 33) { s_count[tid] = 0; s_fill[tid] = 0; }
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  for (uint32_t s = tid; s < alphabet; s += blockDim.x) {
+    uint32_t ln = lengths[s];
+    if (ln > 32) s_bad = 1;
+    else if (ln) atomicAdd(&s_count[ln], 1u);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long code = 0;
+    uint32_t idx = 0, ml = 0;
+    for (int ln = 1; ln <= 32; ++ln) {
+      s_fc[ln] = code;
+      s_fi[ln] = idx;
+      code = (code + s_count[ln]) << 1;
+      idx += s_count[ln];
+      if (s_count[ln]) ml = ln;
+    }
+    hdr->kind = 0;
+    hdr->max_len = ml;
+    hdr->ncodes = idx;
+    hdr->lut_bits = LUT_BITS;
+    hdr->alphabet = alphabet;
+    hdr->status = (s_bad || idx > max_codes) ? BH_BAD_ARGUMENT : BH_OK;
+  }
+  __syncthreads();
+  if (hdr->status != BH_OK) return;
+  const unsigned lt = (1u << lane) - 1;
+  for (uint32_t base = 0; base < alphabet; base += blockDim.x) {
+    uint32_t s = base + tid;
+    uint32_t ln = s < alphabet ? lengths[s] : 0;
+    unsigned peers = __match_any_sync(0xffffffffu, ln);
+    uint32_t wrank = __popc(peers & lt);
+    if (lane < 33) {}
+    for (int i = lane; i < 33; i += 32) s_wcnt[warp][i] = 0;
+    __syncwarp();
+    if (ln && wrank == 0) s_wcnt[warp][ln] = __popc(peers);
+    __syncthreads();
+    if (ln) {
+      uint32_t r = s_fill[ln] + wrank;
+      for (int w = 0; w < warp; ++w) r += s_wcnt[w][ln];
+      unsigned long long code = s_fc[ln] + r;
+      uint32_t idx = s_fi[ln] + r;
+      lj[idx] = (uint32_t)(code << (32 - ln));
+      ljsym[idx] = (uint16_t)s;
+      ljlen[idx] = (uint8_t)ln;
+      if (codes_out) codes_out[s] = (uint32_t)code;
+    } else if (codes_out && s < alphabet) {
+      codes_out[s] = 0;
+    }
+    __syncthreads();
+    if (tid < 33 && tid > 0) {
+      uint32_t add = 0;
+      for (int w = 0; w < 32; ++w) add += s_wcnt[w][tid];
+      s_fill[tid] += add;
+    }
+    __syncthreads();
+  }
+}
+
+// Explicit books: rank every codeword by its left-justified code (codes of a
+// prefix-free book are distinct once left-justified).  O(n^2) over a
+// shared-memory tile; explicit books are small (container cannot carry them,
+// SURVEY A15).
+__global__ void k_explicit_rank(const uint32_t* __restrict__ codes, const uint8_t* __restrict__ lens,
+                                uint32_t alphabet, void* blob, uint32_t max_codes) {
+  TableHdr* hdr; uint32_t* lut; uint16_t* cnt; uint32_t* lj; uint16_t* ljsym; uint8_t* ljlen;
+  table_ptrs(blob, max_codes, hdr, lut, cnt, lj, ljsym, ljlen);
+  __shared__ uint32_t s_key[1024];
+  __shared__ uint8_t s_ok[1024];
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t my_len = i < alphabet ? lens[i] : 0;
+  uint32_t my_key = my_len ? (codes[i] << (32 - my_len)) : 0;
+  uint32_t rank = 0;
+  for (uint32_t base = 0; base < alphabet; base += 1024) {
+    uint32_t j = base + threadIdx.x;
+    uint32_t l2 = j < alphabet ? lens[j] : 0;
+    s_ok[threadIdx.x] = l2 != 0;
+    s_key[threadIdx.x] = l2 ? (codes[j] << (32 - l2)) : 0;
+    __syncthreads();
+    uint32_t lim = min(1024u, alphabet - base);
+    if (my_len)
+      for (uint32_t k = 0; k < lim; ++k) rank += (s_ok[k] && s_key[k] < my_key) ? 1u : 0u;
+    __syncthreads();
+  }
+  if (my_len && rank < max_codes) {
+    lj[rank] = my_key;
+    ljsym[rank] = (uint16_t)i;
+    ljlen[rank] = (uint8_t)my_len;
+  }
+}
+
+__global__ void k_explicit_hdr(const uint8_t* __restrict__ lens, uint32_t alphabet, void* blob,
+                               uint32_t max_codes) {
+  TableHdr* hdr; uint32_t* lut; uint16_t* cnt; uint32_t* lj; uint16_t* ljsym; uint8_t* ljlen;
+  table_ptrs(blob, max_codes, hdr, lut, cnt, lj, ljsym, ljlen);
+  __shared__ uint32_t s_n, s_ml, s_bad;
+  if (threadIdx.x == 0) { s_n = 0; s_ml = 0; s_bad = 0; }
+  __syncthreads();
+  for (uint32_t s = threadIdx.x; s < alphabet; s += blockDim.x) {
+    uint32_t ln = lens[s];
+    if (ln) { atomicAdd(&s_n, 1u); atomicMax(&s_ml, ln); }
+    if (ln > 32) s_bad = 1;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    hdr->kind = 1;
+    hdr->max_len = s_ml;
+    hdr->ncodes = s_n;
+    hdr->lut_bits = LUT_BITS;
+    hdr->alphabet = alphabet;
+    hdr->status = (s_bad || s_n > max_codes) ? BH_BAD_ARGUMENT : BH_OK;
+  }
+}
+
+// First-level tables from the sorted long-code arrays (one CTA).
+__global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_codes) {
+  TableHdr* hdr; uint32_t* lut; uint16_t* cnt; uint32_t* lj; uint16_t* ljsym; uint8_t* ljlen;
+  table_ptrs(blob, max_codes, hdr, lut, cnt, lj, ljsym, ljlen);
+  __shared__ uint32_t s_lut[LUT_SIZE];
+  if (hdr->status != BH_OK) return;
+  TableView t = table_view(blob, max_codes, hdr->ncodes);
+  for (int v = threadIdx.x; v < LUT_SIZE; v += blockDim.x) {
+    uint32_t win = (uint32_t)v << (32 - LUT_BITS);
+    uint32_t e = slow_lookup(t, win);
+    uint32_t len = (e >> 16) & 0xff;
+    if (len > (uint32_t)LUT_BITS) e = 0;  // long code: needs more than the window
+    s_lut[v] = e;
+    lut[v] = e;
+  }
+  __syncthreads();
+  for (int v = threadIdx.x; v < LUT_SIZE; v += blockDim.x) {
+    uint32_t pos = 0, n = 0;
+    while (pos < (uint32_t)LUT_BITS) {
+      uint32_t idx = (uint32_t)((v << pos) & (LUT_SIZE - 1));
+      uint32_t e = s_lut[idx];
+      uint32_t len = (e >> 16) & 0xff;
+      if (len == 0 || pos + len > (uint32_t)LUT_BITS) break;
+      pos += len;
+      ++n;
+    }
+    cnt[v] = n ? (uint16_t)(pos | (n << 8)) : (uint16_t)0;
+  }
+}
+
+}  // namespace bh
+
+using namespace bh;
+
+static int cuda_status(cudaError_t e) { return e == cudaSuccess ? BH_OK : BH_CUDA_ERROR; }
+
+extern "C" size_t bh_table_bytes(uint32_t max_codes) { return TableLayout(max_codes).total; }
+
+extern "C" int bh_table_build(const uint8_t* lengths_dev, uint32_t alphabet, void* table_dev,
+                              uint32_t max_codes, void* cuda_stream) {
+  if (!table_dev || (alphabet && !lengths_dev) || alphabet > 65536u || max_codes > 65536u)
+    return BH_BAD_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  k_canonical<<<1, 1024, 0, st>>>(lengths_dev, alphabet, table_dev, max_codes, nullptr);
+  k_fill_luts<<<1, 1024, 0, st>>>(table_dev, max_codes);
+  return cuda_status(cudaGetLastError());
+}
+
+extern "C" int bh_canonical_codes(const uint8_t* lengths_dev, uint32_t alphabet, uint32_t* codes_dev,
+                                  void* cuda_stream) {
+  if (!codes_dev || alphabet > 65536u) return BH_BAD_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  // scratch blob sized for the full alphabet
+  void* blob = nullptr;
+  size_t bytes = TableLayout(alphabet).total;
+  if (cudaMallocAsync(&blob, bytes, st) != cudaSuccess) return BH_CUDA_ERROR;
+  k_canonical<<<1, 1024, 0, st>>>(lengths_dev, alphabet, blob, alphabet, codes_dev);
+  cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(blob, st);
+  return cuda_status(e);
+}
+
+extern "C" int bh_table_build_explicit(const uint32_t* codes_dev, const uint8_t* lens_dev,
+                                       uint32_t alphabet, void* table_dev, uint32_t max_codes,
+                                       void* cuda_stream) {
+  if (!table_dev || alphabet > 65536u || max_codes > 65536u) return BH_BAD_ARGUMENT;
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  k_explicit_hdr<<<1, 1024, 0, st>>>(lens_dev, alphabet, table_dev, max_codes);
+  if (alphabet) {
+    uint32_t grid = (alphabet + 1023) / 1024;
+    k_explicit_rank<<<grid, 1024, 0, st>>>(codes_dev, lens_dev, alphabet, table_dev, max_codes);
+  }
+  k_fill_luts<<<1, 1024, 0, st>>>(table_dev, max_codes);
+  return cuda_status(cudaGetLastError());
+}
