@@ -195,7 +195,7 @@ extern "C" int bh_decode_async(const bh_stream* s, int variant, const bh_tune* t
                                void* ws, size_t ws_bytes, void* report_dev, void* cuda_stream) {
   if (!s || !s->subseq_bits || !s->subseqs_per_seq || !s->table_dev || !report_dev) return BH_BAD_ARGUMENT;
   if (variant != BH_VARIANT_GAP && variant != BH_VARIANT_SYNC) return BH_BAD_ARGUMENT;
-  if (variant == BH_VARIANT_GAP && !s->gap_dev) return BH_NOTPRESENT;
+  if (variant == BH_VARIANT_GAP && !s->gap_dev && s->total_bits) return BH_NOTPRESENT;
   int rc = bh_report_init(report_dev, cuda_stream);
   if (rc) return rc;
   if (s->total_bits == 0) {
@@ -230,8 +230,8 @@ extern "C" int bh_decode(const bh_stream* s, int variant, const bh_tune* tune, u
     if ((rc = staged_pipeline(s, variant, tune, out_dev, ws, need, rep, cuda_stream, true))) return rc;
     if ((rc = bh_report_read(rep, &r, cuda_stream))) return rc;
     r.repair_needed = 1;
-  } else if (r.status == BH_OK && variant == BH_VARIANT_SYNC && !use_fused(s, variant, tune) &&
-             nseq_of(s) > 1 && s->total_bits) {
+  } else if ((r.status == BH_OK || r.status == BH_TRUNCATED) && variant == BH_VARIANT_SYNC &&
+             !use_fused(s, variant, tune) && nseq_of(s) > 1 && s->total_bits) {
     // staged async pipeline: the final pre-launched seam check must be clean
     Ws L(s, tune);
     int passes = tune && tune->seam_passes ? (int)tune->seam_passes : 2;

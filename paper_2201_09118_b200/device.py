@@ -21,6 +21,8 @@ def h2d(arr: np.ndarray, device, pinned: bool = False):
     """numpy -> device tensor (uint16/uint32 travel as int16/int32 views)."""
     torch = require_cuda()
     a = np.ascontiguousarray(arr)
+    if not a.flags.writeable:
+        a = a.copy()
     view = {np.dtype(np.uint16): np.int16, np.dtype(np.uint32): np.int32,
             np.dtype(np.uint64): np.int64}.get(a.dtype)
     if view is not None:
@@ -85,7 +87,10 @@ class DeviceStream:
                 units = h2d(stream.units, self.device, pinned)
                 check(lib.bh_repack_units(ptr(units), len(stream.units), lay.unit_bits,
                                           ptr(self.words), nwords, st), "repack units")
-        self.gap = h2d(stream.gap, self.device, pinned) if stream.gap is not None else None
+        self.gap = None
+        if stream.gap is not None:
+            g = stream.gap if len(stream.gap) else np.zeros(1, np.uint8)
+            self.gap = h2d(g, self.device, pinned)
         book = stream.codebook
         self.max_codes = max(len(book.entries), 1)
         self.table = empty(lib.bh_table_bytes(self.max_codes), np.uint8, self.device)

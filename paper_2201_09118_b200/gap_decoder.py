@@ -40,6 +40,10 @@ def count_pass(stream, state: SyncState, workers: int = 1, stats: DecodeStats | 
     """Count each slot's codewords between consecutive entries; returns the output index."""
     ns = stream.num_subseqs
     if ns == 0:
+        if stats is not None:
+            stats.add_bits("count_pass", 0)
+        if stream.symbol_count:
+            raise BadGap(f"gap entries give 0 symbols; the header says {stream.symbol_count}")
         return np.zeros(1, np.int64)
     ds = device_stream(stream)
     dev = ds.device
