@@ -116,6 +116,11 @@ int bh_report_read(const void *report_dev, bh_report *report_host, void *cuda_st
 /* workspace bh_decode needs: bh_workspace_bytes() plus room for its report */
 size_t bh_decode_workspace_bytes(const bh_stream *s, int variant, const bh_tune *tune);
 
+/* ---- phase profiler (CUDA events around every phase on the caller's stream) */
+int bh_profile_enable(int on);
+/* aggregated per phase: names newline-separated, summed ms, interval counts */
+int bh_profile_read(char *names, size_t names_len, float *ms, uint32_t *count, int cap);
+
 /* ---- sub-steps with the reference's SyncState arrays (state.py:16-41) --- */
 /* int64 entries/exits/counts[num_subseqs], uint8 synced, int32 iterations[num_seqs] */
 int bh_intra_sync(const bh_stream *s, int early_exit, int64_t *entries_dev, int64_t *exits_dev,
@@ -164,6 +169,8 @@ int bh_decode_write_classes(const bh_stream *s, const int64_t *entries_dev, cons
                             uint64_t nseq_ids, uint32_t capacity, uint32_t max_capacity,
                             const int64_t *classes_dev, const uint32_t *caps_dev, uint16_t *out_dev,
                             uint64_t out_len, void *report_dev, int stats, void *cuda_stream);
+/* per-class capacities copied through the launch (n <= 256) */
+int bh_fill_caps(uint32_t *caps_dev, const uint32_t *caps_host, uint32_t n, void *cuda_stream);
 /* header check: out_index_dev[num_subseqs] vs symbol_count */
 int bh_check_total(const bh_stream *s, const int64_t *out_index_dev, int status_on_mismatch,
                    void *report_dev, void *cuda_stream);

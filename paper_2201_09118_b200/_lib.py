@@ -89,6 +89,9 @@ SIGNATURES = {
     "bh_sequential_decode": (I32, [P, U64, U64, I32, P, P, P, P]),
     "bh_start_histogram": (I32, [P, U64, U32, P, U64, P]),
     "bh_coarse_decode": (I32, [P, P, U64, P, P, P]),
+    "bh_profile_enable": (I32, [I32]),
+    "bh_profile_read": (I32, [C.c_char_p, SZ, P, P, I32]),
+    "bh_fill_caps": (I32, [P, P, U32, P]),
 }
 
 _lib = None
@@ -156,3 +159,20 @@ def stream_handle(torch_stream=None) -> int:
     import torch
     st = torch_stream or torch.cuda.current_stream()
     return st.cuda_stream
+
+
+def profile_enable(on: bool = True) -> None:
+    check(load().bh_profile_enable(1 if on else 0), "profile")
+
+
+def profile_read() -> dict:
+    """{phase: (total_ms, intervals)} accumulated since profile_enable()."""
+    import numpy as np
+    names = C.create_string_buffer(4096)
+    ms = np.zeros(64, np.float32)
+    cnt = np.zeros(64, np.uint32)
+    n = load().bh_profile_read(names, 4096, ms.ctypes.data, cnt.ctypes.data, 64)
+    if n < 0:
+        raise RuntimeError("profile read failed")
+    keys = names.value.decode().split("\n")[:n]
+    return {k: (float(ms[i]), int(cnt[i])) for i, k in enumerate(keys)}

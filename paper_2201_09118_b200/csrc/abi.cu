@@ -24,6 +24,7 @@ int bh_decode_write_classes(const bh_stream* s, const int64_t* entries_dev, cons
 int bh_seam_check(const bh_stream* s, const int64_t* entries_dev, const int64_t* exits_dev,
                   int64_t* seeds_dev, unsigned long long* counter_dev, void* cuda_stream);
 int bh_fused_supported(const bh_stream* s, int variant);
+int bh_fill_caps(uint32_t* caps_dev, const uint32_t* caps_host, uint32_t n, void* cuda_stream);
 size_t bh_fused_workspace_bytes(const bh_stream* s, int variant, const bh_tune* tune);
 int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* tune, uint16_t* out_dev,
                     void* ws, size_t ws_bytes, void* report_dev, void* cuda_stream);
@@ -84,6 +85,75 @@ T* at(void* ws, size_t off) { return reinterpret_cast<T*>(static_cast<char*>(ws)
 
 extern "C" int bh_version(void) { return 100; }
 
+// ---- phase profiler ---------------------------------------------------------
+// Every decoder phase is bracketed by CUDA events recorded on the launching
+// stream (prof_mark).  bh_profile_read aggregates the elapsed time between
+// consecutive marks per phase name; the interval ending at a "start" mark
+// (whatever ran between two decodes, e.g. an L2 flush) is dropped.
+namespace {
+constexpr int PROF_MAX = 8192;
+cudaEvent_t g_ev[PROF_MAX];
+const char* g_name[PROF_MAX];
+int g_nev = 0;
+bool g_prof = false;
+bool g_ev_made = false;
+}  // namespace
+
+void bh::prof_mark(cudaStream_t st, const char* phase) {
+  if (!g_prof || g_nev >= PROF_MAX) return;
+  cudaEventRecord(g_ev[g_nev], st);
+  g_name[g_nev] = phase;
+  ++g_nev;
+}
+
+extern "C" int bh_profile_enable(int on) {
+  if (on && !g_ev_made) {
+    for (int i = 0; i < PROF_MAX; ++i)
+      if (cudaEventCreate(&g_ev[i]) != cudaSuccess) return BH_CUDA_ERROR;
+    g_ev_made = true;
+  }
+  g_prof = on != 0;
+  g_nev = 0;
+  return BH_OK;
+}
+
+// names: newline-separated phase names; ms: summed milliseconds; count: number
+// of intervals per phase.  Returns the number of distinct phases (<= cap).
+extern "C" int bh_profile_read(char* names, size_t names_len, float* ms, uint32_t* count, int cap) {
+  if (names_len) names[0] = 0;
+  if (g_nev < 2) { g_nev = 0; return 0; }
+  if (cudaEventSynchronize(g_ev[g_nev - 1]) != cudaSuccess) return -BH_CUDA_ERROR;
+  const char* uniq[64];
+  int nu = 0;
+  for (int i = 1; i < g_nev; ++i) {
+    if (!strcmp(g_name[i], "start")) continue;
+    int k = 0;
+    while (k < nu && strcmp(uniq[k], g_name[i])) ++k;
+    if (k == nu) {
+      if (nu >= cap || nu >= 64) continue;
+      uniq[nu] = g_name[i];
+      ms[nu] = 0.f;
+      count[nu] = 0;
+      ++nu;
+    }
+    float t = 0.f;
+    cudaEventElapsedTime(&t, g_ev[i - 1], g_ev[i]);
+    ms[k] += t;
+    count[k] += 1;
+  }
+  size_t used = 0;
+  for (int k = 0; k < nu; ++k) {
+    size_t l = strlen(uniq[k]);
+    if (used + l + 2 >= names_len) break;
+    memcpy(names + used, uniq[k], l);
+    used += l;
+    names[used++] = '\n';
+    names[used] = 0;
+  }
+  g_nev = 0;
+  return nu;
+}
+
 static bool use_fused(const bh_stream* s, int variant, const bh_tune* tune) {
   return (!tune || tune->fused) && bh_fused_supported(s, variant);
 }
@@ -122,13 +192,17 @@ static int staged_pipeline(const bh_stream* s, int variant, const bh_tune* tune,
   int64_t* oi = at<int64_t>(ws, L.oi);
   const int stats = tune && tune->collect_stats;
   int rc;
+  prof_mark(S(st), "start");
   if (variant == BH_VARIANT_GAP) {
     if ((rc = bh_entries_from_gap(s, entries, st))) return rc;
+    prof_mark(S(st), "entries_from_gap");
     if ((rc = bh_count_windows(s, 1, entries, counts, exits, rep, st))) return rc;
+    prof_mark(S(st), "count_pass");
   } else {
     if ((rc = bh_intra_sync_ex(s, nullptr, 0, nullptr, entries, exits, counts, at<uint8_t>(ws, L.synced),
                                at<int32_t>(ws, L.iters), at<void>(ws, L.flags), 2 * ns + 8 * nq + 16, rep, st)))
       return rc;
+    prof_mark(S(st), "intra_sync");
     unsigned long long* ctr = at<unsigned long long>(ws, L.seam_ctr);
     int64_t* seeds = at<int64_t>(ws, L.seeds);
     if (nq > 1) {
@@ -162,9 +236,11 @@ static int staged_pipeline(const bh_stream* s, int variant, const bh_tune* tune,
         if ((rc = bh_seam_check(s, entries, exits, seeds, ctr + passes, st))) return rc;
       }
     }
+    prof_mark(S(st), "inter_sync");
   }
   if ((rc = bh_output_index(counts, ns, oi, at<void>(ws, L.scan), bh_scan_workspace_bytes(ns), st))) return rc;
   if ((rc = bh_check_total(s, oi, variant == BH_VARIANT_GAP ? BH_BADGAP : BH_TRUNCATED, rep, st))) return rc;
+  prof_mark(S(st), "output_index");
   if (tune && tune->t_high) {
     const uint32_t C = tune->t_high + 1;
     int64_t* seqc = at<int64_t>(ws, L.seqc);
@@ -180,15 +256,19 @@ static int staged_pipeline(const bh_stream* s, int variant, const bh_tune* tune,
       if (caps[c - 1] > maxcap) maxcap = caps[c - 1];
     }
     uint32_t* caps_dev = at<uint32_t>(ws, L.caps);
-    if (cudaMemcpyAsync(caps_dev, caps, 4 * C, cudaMemcpyHostToDevice, S(st)) != cudaSuccess) return BH_CUDA_ERROR;
-    if (cudaStreamSynchronize(S(st)) != cudaSuccess) return BH_CUDA_ERROR;  // caps lives on our stack
-    return bh_decode_write_classes(s, entries, counts, oi, at<int64_t>(ws, L.perm), nq, 0, maxcap,
-                                   at<int64_t>(ws, L.classes), caps_dev, out, s->symbol_count, rep,
-                                   stats, st);
+    if ((rc = bh_fill_caps(caps_dev, caps, C, st))) return rc;
+    prof_mark(S(st), "tune");
+    rc = bh_decode_write_classes(s, entries, counts, oi, at<int64_t>(ws, L.perm), nq, 0, maxcap,
+                                 at<int64_t>(ws, L.classes), caps_dev, out, s->symbol_count, rep,
+                                 stats, st);
+    prof_mark(S(st), "decode_write");
+    return rc;
   }
   uint32_t cap = tune && tune->capacity ? tune->capacity : 3584;
-  return bh_decode_write_classes(s, entries, counts, oi, nullptr, nq, cap, cap, nullptr, nullptr, out,
-                                 s->symbol_count, rep, stats, st);
+  rc = bh_decode_write_classes(s, entries, counts, oi, nullptr, nq, cap, cap, nullptr, nullptr, out,
+                               s->symbol_count, rep, stats, st);
+  prof_mark(S(st), "decode_write");
+  return rc;
 }
 
 extern "C" int bh_decode_async(const bh_stream* s, int variant, const bh_tune* tune, uint16_t* out_dev,

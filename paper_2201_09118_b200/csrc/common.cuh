@@ -186,6 +186,11 @@ struct DevReport {
   unsigned long long pad[4];
 };
 
+// Host-side phase profiler (abi.cu): when enabled, every decoder phase is
+// bracketed by CUDA events on the launching stream (bh_profile_enable /
+// bh_profile_read); costs nothing when disabled.
+void prof_mark(cudaStream_t st, const char* phase);
+
 __device__ __forceinline__ void report_error(DevReport* rep, int status, uint64_t slot) {
   // lowest status code wins (INVALID=1 < TRUNCATED=2 < BADGAP=3 ...), matching
   // the reference where InvalidCode surfaces before header-count checks.

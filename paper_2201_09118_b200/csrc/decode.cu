@@ -875,3 +875,19 @@ extern "C" int bh_start_histogram(const int64_t* starts_dev, uint64_t n, uint32_
       starts_dev, n, subseq_bits, reinterpret_cast<unsigned long long*>(counts_dev));
   return last_status();
 }
+
+namespace bh {
+struct Caps { uint32_t v[256]; };
+__global__ void k_fill_caps(uint32_t* __restrict__ dst, Caps caps, uint32_t n) {
+  for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = caps.v[i];
+}
+}  // namespace bh
+
+// per-class capacities (host array, copied by value through the launch)
+extern "C" int bh_fill_caps(uint32_t* caps_dev, const uint32_t* caps_host, uint32_t n, void* cuda_stream) {
+  if (n > 256) return BH_BAD_ARGUMENT;
+  Caps c;
+  for (uint32_t i = 0; i < n; ++i) c.v[i] = caps_host[i];
+  k_fill_caps<<<1, 256, 0, S(cuda_stream)>>>(caps_dev, c, n);
+  return last_status();
+}
