@@ -169,6 +169,8 @@ class Decoder:
         self.out = empty(stream.symbol_count, np.uint16, self.ds.device)
         self.wsb = self.lib.bh_workspace_bytes(self.ds.ref, self.variant, C.byref(self.tune))
         self.ws = torch.empty(max(self.wsb, 256), dtype=torch.uint8, device=self.ds.device)
+        from paper_2201_09118_b200._lib import stream_handle
+        self.lib.bh_workspace_reset(self.ws.data_ptr(), self.ws.numel(), stream_handle())
         self.rep = DeviceReport(self.ds.device)
 
     def __call__(self):
@@ -243,6 +245,7 @@ def e2e_measure(stream, book, variant: str, steps: int, flush):
     tune = make_tune()
     wsb = lib.bh_workspace_bytes(C.byref(cs), var, C.byref(tune))
     ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)
+    lib.bh_workspace_reset(ws.data_ptr(), ws.numel(), stream_handle())
     rep = DeviceReport(dev)
 
     def step():

@@ -30,6 +30,7 @@ extern "C" {
 #define BH_GAPOVERFLOW 6   /* GapOverflow (encoder.py:86-87) */
 #define BH_BAD_ARGUMENT 7  /* ValueError-class misuse (layout, capacity < 1, ...) */
 #define BH_CUDA_ERROR 8    /* CUDA runtime failure */
+#define BH_NEED_STAGED 9   /* fused path declined (incomplete codebook); bh_decode reruns staged */
 
 #define BH_VARIANT_GAP 1     /* gap_decoder.decode (gap_decoder.py:71-92) */
 #define BH_VARIANT_SYNC 2    /* sync_decoder.decode (sync_decoder.py:173-211) */
@@ -106,6 +107,9 @@ size_t bh_workspace_bytes(const bh_stream *s, int variant, const bh_tune *tune);
 int bh_decode_async(const bh_stream *s, int variant, const bh_tune *tune, uint16_t *out_dev,
                     void *workspace_dev, size_t workspace_bytes, void *report_dev,
                     void *cuda_stream);
+/* zero a freshly allocated workspace once (descriptors are epoch-tagged, so
+ * later calls need no reset) */
+int bh_workspace_reset(void *workspace_dev, size_t workspace_bytes, void *cuda_stream);
 /* Synchronous convenience: decode, finish any extra seam passes, read report. */
 int bh_decode(const bh_stream *s, int variant, const bh_tune *tune, uint16_t *out_dev,
               void *workspace_dev, size_t workspace_bytes, bh_report *report_host,

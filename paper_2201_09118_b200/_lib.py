@@ -16,7 +16,7 @@ from . import errors
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libb200huff.so"
 
 BH_OK, BH_INVALID, BH_TRUNCATED, BH_BADGAP, BH_NOFIXPOINT = 0, 1, 2, 3, 4
-BH_NOTPRESENT, BH_GAPOVERFLOW, BH_BAD_ARGUMENT, BH_CUDA_ERROR = 5, 6, 7, 8
+BH_NOTPRESENT, BH_GAPOVERFLOW, BH_BAD_ARGUMENT, BH_CUDA_ERROR, BH_NEED_STAGED = 5, 6, 7, 8, 9
 VARIANT_GAP, VARIANT_SYNC, VARIANT_COARSE = 1, 2, 3
 WORD_PAD = 8
 
@@ -92,6 +92,7 @@ SIGNATURES = {
     "bh_profile_enable": (I32, [I32]),
     "bh_profile_read": (I32, [C.c_char_p, SZ, P, P, I32]),
     "bh_fill_caps": (I32, [P, P, U32, P]),
+    "bh_workspace_reset": (I32, [P, SZ, P]),
 }
 
 _lib = None

@@ -213,10 +213,13 @@ static int staged_pipeline(const bh_stream* s, int variant, const bh_tune* tune,
         // sync_decoder.py:129-149 exactly: snapshot, stop when nothing is stale
         for (uint64_t p = 0;; ++p) {
           unsigned long long stale = 0;
+          int32_t dev_status = 0;
           cudaMemsetAsync(ctr, 0, 8, S(st));
           if ((rc = bh_seam_check(s, entries, exits, seeds, ctr, st))) return rc;
           if (cudaMemcpyAsync(&stale, ctr, 8, cudaMemcpyDeviceToHost, S(st)) != cudaSuccess) return BH_CUDA_ERROR;
+          if (cudaMemcpyAsync(&dev_status, rep, 4, cudaMemcpyDeviceToHost, S(st)) != cudaSuccess) return BH_CUDA_ERROR;
           if (cudaStreamSynchronize(S(st)) != cudaSuccess) return BH_CUDA_ERROR;
+          if (dev_status != 0x7fffffff) break;  // an intra/seam decode failed: the report says why
           if (!stale) break;
           if (p >= nq) return BH_NOFIXPOINT;
           if ((rc = bh_intra_sync_ex(s, seeds, 0, ctr, entries, exits, counts, at<uint8_t>(ws, L.synced),
@@ -276,6 +279,8 @@ extern "C" int bh_decode_async(const bh_stream* s, int variant, const bh_tune* t
   if (!s || !s->subseq_bits || !s->subseqs_per_seq || !s->table_dev || !report_dev) return BH_BAD_ARGUMENT;
   if (variant != BH_VARIANT_GAP && variant != BH_VARIANT_SYNC) return BH_BAD_ARGUMENT;
   if (variant == BH_VARIANT_GAP && !s->gap_dev && s->total_bits) return BH_NOTPRESENT;
+  if (s->total_bits && use_fused(s, variant, tune))
+    return bh_fused_decode(s, variant, tune, out_dev, ws, ws_bytes, report_dev, cuda_stream);
   int rc = bh_report_init(report_dev, cuda_stream);
   if (rc) return rc;
   if (s->total_bits == 0) {
@@ -283,8 +288,6 @@ extern "C" int bh_decode_async(const bh_stream* s, int variant, const bh_tune* t
     return bh_check_total(s, nullptr, variant == BH_VARIANT_GAP ? BH_BADGAP : BH_TRUNCATED, report_dev,
                           cuda_stream);
   }
-  if (use_fused(s, variant, tune))
-    return bh_fused_decode(s, variant, tune, out_dev, ws, ws_bytes, report_dev, cuda_stream);
   return staged_pipeline(s, variant, tune, out_dev, ws, ws_bytes, report_dev, cuda_stream, false);
 }
 
@@ -304,8 +307,9 @@ extern "C" int bh_decode(const bh_stream* s, int variant, const bh_tune* tune, u
   bh_report r;
   memset(&r, 0, sizeof(r));
   if ((rc = bh_report_read(rep, &r, cuda_stream))) return rc;
-  if (r.status == BH_OK && r.repair_needed) {
-    // fused sync speculation missed a seam: redo with the exact staged pipeline
+  if (r.status == BH_NEED_STAGED) {
+    // the fused path declined (incomplete codebook): the reference-structured
+    // pipeline reproduces the reference's speculative windows exactly
     if ((rc = bh_report_init(rep, cuda_stream))) return rc;
     if ((rc = staged_pipeline(s, variant, tune, out_dev, ws, need, rep, cuda_stream, true))) return rc;
     if ((rc = bh_report_read(rep, &r, cuda_stream))) return rc;

@@ -30,17 +30,35 @@ struct TableHdr {
   uint32_t lut_bits;
   uint32_t alphabet;
   uint32_t status;    // BH_OK or build error
-  uint32_t pad[10];
+  uint32_t complete;  // Kraft sum == 1: every bit pattern decodes
+  uint32_t pad[9];
 };
+
+// Fused-kernel tables:
+//   dlut8 u32[256]   next 8 bits -> sym | len<<16 for codes of <= 8 bits, else 0
+//   clut8 u8[256]    next 8 bits -> (ncode<<3) | (bits-1) over every whole
+//                    codeword inside the 8 bits, 0 if the first one is longer
+//   lut12 u32[4096]  next 12 bits -> sym | len<<16 for codes of <= 12 bits, else 0
+//   lim   u64[33]    canonical left-justified limit per length
+//   base  i64[33]    first_index - first_code per length
+// The kernel replicates dlut8/clut8 once per lane ("bank-private": lane l only
+// ever touches shared-memory bank l), so table lookups never conflict.
+constexpr int FB = 12;
+constexpr int FB_SIZE = 1 << FB;
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct TableLayout {
-  size_t lut, cnt, lj, ljsym, ljlen, total;
+  size_t lut, cnt, dlut8, clut8, lut12, lim, base, lj, ljsym, ljlen, total;
   __host__ __device__ explicit TableLayout(uint32_t max_codes) {
     lut = TABLE_HDR_BYTES;
     cnt = lut + sizeof(uint32_t) * LUT_SIZE;
-    lj = align16(cnt + sizeof(uint16_t) * LUT_SIZE);
+    dlut8 = align16(cnt + sizeof(uint16_t) * LUT_SIZE);
+    clut8 = dlut8 + 4 * 256;
+    lut12 = align16(clut8 + 256);
+    lim = align16(lut12 + 4 * (size_t)FB_SIZE);
+    base = lim + 8 * 33;
+    lj = align16(base + 8 * 33);
     ljsym = align16(lj + sizeof(uint32_t) * (size_t)max_codes);
     ljlen = align16(ljsym + sizeof(uint16_t) * (size_t)max_codes);
     total = align16(ljlen + (size_t)max_codes);

@@ -65,6 +65,19 @@ __global__ void __launch_bounds__(1024) k_canonical(const uint8_t* __restrict__ 
     hdr->lut_bits = LUT_BITS;
     hdr->alphabet = alphabet;
     hdr->status = (s_bad || idx > max_codes) ? BH_BAD_ARGUMENT : BH_OK;
+    unsigned long long kraft = 0;
+    for (int ln = 1; ln <= 32; ++ln) kraft += (unsigned long long)s_count[ln] << (32 - ln);
+    hdr->complete = kraft == (1ull << 32) ? 1u : 0u;
+    // canonical limits for the fused kernels' long-code path
+    TableLayout L(max_codes);
+    unsigned long long* lim = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(blob) + L.lim);
+    long long* base = reinterpret_cast<long long*>(reinterpret_cast<char*>(blob) + L.base);
+    lim[0] = 0;
+    base[0] = 0;
+    for (int ln = 1; ln <= 32; ++ln) {
+      lim[ln] = (s_fc[ln] + s_count[ln]) << (32 - ln);
+      base[ln] = (long long)s_fi[ln] - (long long)s_fc[ln];
+    }
   }
   __syncthreads();
   if (hdr->status != BH_OK) return;
@@ -138,12 +151,14 @@ __global__ void k_explicit_hdr(const uint8_t* __restrict__ lens, uint32_t alphab
   TableHdr* hdr; uint32_t* lut; uint16_t* cnt; uint32_t* lj; uint16_t* ljsym; uint8_t* ljlen;
   table_ptrs(blob, max_codes, hdr, lut, cnt, lj, ljsym, ljlen);
   __shared__ uint32_t s_n, s_ml, s_bad;
-  if (threadIdx.x == 0) { s_n = 0; s_ml = 0; s_bad = 0; }
+  __shared__ unsigned long long s_kraft;
+  if (threadIdx.x == 0) { s_n = 0; s_ml = 0; s_bad = 0; s_kraft = 0; }
   __syncthreads();
   for (uint32_t s = threadIdx.x; s < alphabet; s += blockDim.x) {
     uint32_t ln = lens[s];
     if (ln) { atomicAdd(&s_n, 1u); atomicMax(&s_ml, ln); }
     if (ln > 32) s_bad = 1;
+    else if (ln) atomicAdd(&s_kraft, 1ull << (32 - ln));
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -153,6 +168,7 @@ __global__ void k_explicit_hdr(const uint8_t* __restrict__ lens, uint32_t alphab
     hdr->lut_bits = LUT_BITS;
     hdr->alphabet = alphabet;
     hdr->status = (s_bad || s_n > max_codes) ? BH_BAD_ARGUMENT : BH_OK;
+    hdr->complete = s_kraft == (1ull << 32) ? 1u : 0u;
   }
 }
 
@@ -183,6 +199,29 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
       ++n;
     }
     cnt[v] = n ? (uint16_t)(pos | (n << 8)) : (uint16_t)0;
+  }
+  // tables for the fused kernels
+  TableLayout L(max_codes);
+  uint32_t* dlut8 = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(blob) + L.dlut8);
+  uint8_t* clut8 = reinterpret_cast<uint8_t*>(reinterpret_cast<char*>(blob) + L.clut8);
+  uint32_t* lut12 = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(blob) + L.lut12);
+  for (int v = threadIdx.x; v < FB_SIZE; v += blockDim.x) {
+    uint32_t e = slow_lookup(t, (uint32_t)v << (32 - FB));
+    lut12[v] = ((e >> 16) & 0xff) <= (uint32_t)FB ? e : 0u;
+  }
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) {
+    uint32_t e = slow_lookup(t, (uint32_t)v << 24);
+    dlut8[v] = ((e >> 16) & 0xff) <= 8u ? e : 0u;
+    uint32_t pos = 0, n = 0;
+    while (pos < 8) {
+      uint32_t w = ((uint32_t)v << 24) << pos;  // zero-filled past the window
+      uint32_t f = slow_lookup(t, w);
+      uint32_t len = (f >> 16) & 0xff;
+      if (len == 0 || pos + len > 8) break;
+      pos += len;
+      ++n;
+    }
+    clut8[v] = n ? (uint8_t)((n << 3) | (pos - 1)) : (uint8_t)0;
   }
 }
 

@@ -63,6 +63,8 @@ class Workspace:
         buf = cls._bufs.get(key)
         if buf is None or buf.numel() < nbytes:
             buf = torch.empty(max(int(nbytes), 256) + 256, dtype=torch.uint8, device=device)
+            # fused-kernel descriptors are epoch-tagged: zero once per allocation
+            check(load().bh_workspace_reset(buf.data_ptr(), buf.numel(), stream_handle()), "workspace")
             cls._bufs[key] = buf
         return buf
 

@@ -66,3 +66,30 @@ def test_sync_points_sound(ph, oracle_mod):
         assert np.array_equal(state.iterations, ref.iterations)
         starts = np.append(orc.starts, st.total_bits)
         assert np.isin(state.entry_bits, starts).all()
+
+
+@pytest.mark.parametrize("cap,warps", [("256", "4"), ("512", "8"), ("1024", "32"), ("", "1")])
+def test_fused_staging_rounds_and_bypass(ph, oracle_mod, monkeypatch, cap, warps):
+    """Small staging capacities force the fused kernel into the reference's
+    round/straddler/bypass rule; the output must not change."""
+    if cap:
+        monkeypatch.setenv("BH_FUSED_CAP", cap)
+    monkeypatch.setenv("BH_FUSED_WARPS", warps)
+    rng = np.random.default_rng(int(cap or 0) + int(warps))
+    for sharp, n in ((0.999, 300_000), (0.9, 200_000), (0.3, 100_000)):
+        syms, _ = case_symbols(rng, 0, n)
+        from streams import synth_codes
+        syms = synth_codes(n, sharp, int(rng.integers(1 << 30)))
+        st = ph.encode(syms, ph.book_for(syms, 16), ph.DEFAULT_LAYOUT, with_gap=True)
+        assert np.array_equal(ph.gap_decoder.decode(st), syms)
+        assert np.array_equal(ph.sync_decoder.decode(st), syms)
+
+
+def test_fused_matches_staged_on_layouts(ph):
+    rng = np.random.default_rng(77)
+    for lay in ((32, 4, 32), (16, 3, 5), (8, 5, 7), (32, 1, 32), (32, 8, 16), (8, 1, 32), (32, 2, 3)):
+        for _ in range(3):
+            syms, width = case_symbols(rng, int(rng.integers(0, 100)), int(rng.integers(1, 80_000)))
+            st = ph.encode(syms, ph.book_for(syms, width), ph.LayoutConfig(*lay), with_gap=True)
+            assert np.array_equal(ph.gap_decoder.decode(st), syms), lay
+            assert np.array_equal(ph.sync_decoder.decode(st), syms), lay
