@@ -74,16 +74,15 @@ struct FusedArgs {
   DevReport* rep;
   uint32_t epoch;
   uint32_t wpb;          // words per tile buffer (multiple of 4)
-  uint32_t row_words;    // staging row stride in words (odd)
+  uint32_t cap;          // staging symbols per warp (multiple of 8)
   uint32_t warps;        // warps per CTA
   uint32_t per_warp_bytes;
   uint32_t tables_bytes;
 };
 
 // shared-memory table layout inside the CTA (bytes)
-constexpr uint32_t T_DL = 0;                      // u32 [256][32] replicated dlut8
-constexpr uint32_t T_CL = T_DL + 256 * 32 * 4;    // u8  [64][32][4] replicated clut8
-constexpr uint32_t T_LIM = T_CL + 256 * 32;       // u64 [33]
+constexpr uint32_t T_WL = 0;                      // uint2 [256][32] replicated wlut8
+constexpr uint32_t T_LIM = T_WL + 256 * 32 * 8;   // u64 [33]
 constexpr uint32_t T_BASE = T_LIM + 33 * 8;       // i64 [33]
 constexpr uint32_t T_END = T_BASE + 33 * 8;
 
@@ -119,8 +118,8 @@ __device__ __forceinline__ uint32_t lds8(uint32_t a) {
   asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
   return v;
 }
-__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
-  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
+__device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
 }
 
 // Keep a value in a register: the compiler may not rematerialise it (it
@@ -154,8 +153,7 @@ struct SR {
 };
 
 struct FTab {
-  uint32_t dl;     // this lane's column of the replicated dlut8 (shared address)
-  uint32_t cl;     // this lane's column of the replicated clut8
+  uint32_t wl;     // this lane's column of the replicated wlut8 (shared address)
   uint32_t lim;    // shared address of lim (u64[33])
   uint32_t base;   // shared address of base (i64[33])
   TableView t;
@@ -168,7 +166,7 @@ __device__ __noinline__ uint32_t fslow(uint32_t win, const uint32_t lim_s, const
   if (kind == 0) {
     const uint2 l32 = lds64(lim_s + 32 * 8);
     if ((unsigned long long)win >= (((unsigned long long)l32.y << 32) | l32.x)) return 0;
-    uint32_t lo = 9, hi = 32;  // codes of <= 8 bits are answered by dlut8
+    uint32_t lo = 1, hi = 32;
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
       const uint2 l = lds64(lim_s + mid * 8);
@@ -183,88 +181,101 @@ __device__ __noinline__ uint32_t fslow(uint32_t win, const uint32_t lim_s, const
 
 // one codeword: sym | len<<16 (0 = no codeword matches)
 __device__ __forceinline__ uint32_t fone(uint32_t win, const FTab& T) {
-  uint32_t e = lds32(T.dl + ((win >> 24) << 7));
-  if (!e) e = fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t);
-  return e;
+  const uint2 w = lds64(T.wl + ((win >> 24) << 8));
+  if (w.y) return (w.x & 0xffffu) | ((((w.y >> 21) & 7u) + 1) << 16);
+  return fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t);
+}
+
+__device__ __forceinline__ uint32_t flen(uint32_t win, const FTab& T) {
+  const uint32_t y = lds32(T.wl + ((win >> 24) << 8) + 4);
+  if (y) return ((y >> 21) & 7u) + 1;
+  return (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t) >> 16) & 0xffu;
 }
 
 // count codewords starting in [pos, stop) (tile-relative); pos ends at the exit
 __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, const FTab& T, uint32_t& n) {
-  while (pos < stop) {
+  const uint32_t wy = pin(T.wl + 4);
+  while (pos + 8 <= stop) {  // every whole codeword of the next 8 bits starts before stop
     const uint32_t win = r.peek();
-    if (stop - pos >= 8u) {
-      const uint32_t c = lds8(T.cl + ((win >> 26) << 7) + ((win >> 24) & 3));
-      if (c) {
-        const uint32_t b = (c & 7u) + 1;
-        n += c >> 3;
-        r.skip(b);
-        pos += b;
-        continue;
-      }
-    }
-    const uint32_t len = (fone(win, T) >> 16) & 0xffu;
+    const uint32_t y = lds32(wy + ((win >> 24) << 8));
+    if (!y) break;
+    const uint32_t b = (y >> 28) + 1;
+    n += (y >> 24) & 15u;
+    r.skip(b);
+    pos += b;
+  }
+  while (pos < stop) {
+    const uint32_t len = flen(r.peek(), T);
     if (!len) return false;
     r.skip(len);
     pos += len;
     ++n;
+    if (pos + 8 <= stop) {  // back to the multi-codeword path after a long code
+      while (pos + 8 <= stop) {
+        const uint32_t win = r.peek();
+        const uint32_t y = lds32(wy + ((win >> 24) << 8));
+        if (!y) break;
+        const uint32_t b = (y >> 28) + 1;
+        n += (y >> 24) & 15u;
+        r.skip(b);
+        pos += b;
+      }
+    }
   }
   return true;
 }
 
-// Decode c symbols into this lane's staging row (pairs of symbols per word).
-// Lanes step in lock-step (same pair index), so lane l's store lands in bank
-// (row_words*l + p) mod 32 -- distinct for the odd row_words.  The reader is
-// topped up 16 bits at a time so that both lookups of a pair need no refill:
-// with >= 48 valid bits at the top of a pair, two codes of <= 8 bits leave
-// >= 32; a longer code takes the slow path, which refills as it goes.
-__device__ __forceinline__ bool fdecode_row(const SR& r0, uint32_t c, uint32_t row, uint32_t wbuf_s,
-                                            const FTab& T) {
-  bool ok = true;
-  const uint32_t dl = pin(T.dl);
-  uint64_t buf = r0.buf;
-  uint32_t av = r0.av;
-  uint32_t ha = (r0.wa - wbuf_s) >> 1;  // next halfword of the MSB-first word stream
-#define BH_TOPUP()                                          \
-  {                                                         \
-    const uint32_t h_ = lds16(wbuf_s + ((ha ^ 1u) << 1));   \
-    buf |= (uint64_t)h_ << (48 - av);                       \
-    av += 16;                                               \
-    ++ha;                                                   \
-  }
-  for (uint32_t k = 0; k < c; k += 2) {
-    if (av < 48) BH_TOPUP();
-    const uint32_t w0 = (uint32_t)(buf >> 32);
-    const uint32_t e0 = lds32(dl + ((w0 >> 24) << 7));
-    const uint32_t l0 = e0 >> 16;
-    const uint32_t w1 = (uint32_t)((buf << l0) >> 32);
-    const uint32_t e1 = lds32(dl + ((w1 >> 24) << 7));
-    uint32_t pair;
-    if (e0 && e1) {
-      const uint32_t s = l0 + (e1 >> 16);
-      buf <<= s;
-      av -= s;
-      pair = (e0 & 0xffffu) | (e1 << 16);
+// Decode c (>= 1) symbols into compact staging at `dst` (lane ranges are
+// disjoint; stores past the lane's own range are predicated off).
+__device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const FTab& T) {
+  const uint32_t wl = pin(T.wl);
+  int32_t k = (int32_t)c;
+  while (k > 0) {
+    const uint32_t win = r.peek();
+    const uint2 w = lds64(wl + ((win >> 24) << 8));
+    if (w.y) {
+      const uint32_t n = (w.y >> 16) & 3u;
+      sts16(dst, w.x);
+      if (n > 1 && k > 1) sts16(dst + 2, w.x >> 16);
+      if (n > 2 && k > 2) sts16(dst + 4, w.y);
+      dst += n << 1;
+      k -= (int32_t)n;
+      r.skip(((w.y >> 18) & 7u) + 1);
     } else {
-      // a code longer than 8 bits: one codeword at a time, refilling as needed
-      const uint32_t s0 = fone((uint32_t)(buf >> 32), T);
-      ok = ok && s0;
-      buf <<= (s0 >> 16) & 0xffu;
-      av -= (s0 >> 16) & 0xffu;
-      while (av < 48) BH_TOPUP();
-      uint32_t s1 = 0;
-      if (k + 1 < c) {
-        s1 = fone((uint32_t)(buf >> 32), T);
-        ok = ok && s1;
-        buf <<= (s1 >> 16) & 0xffu;
-        av -= (s1 >> 16) & 0xffu;
-        while (av < 48) BH_TOPUP();
-      }
-      pair = (s0 & 0xffffu) | (s1 << 16);
+      const uint32_t e = fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t);
+      const uint32_t len = (e >> 16) & 0xffu;
+      if (!len) return false;
+      sts16(dst, e);
+      dst += 2;
+      k -= 1;
+      r.skip(len);
     }
-    sts32(row + 2 * k, pair);
   }
-#undef BH_TOPUP
-  return ok;
+  return true;
+}
+
+// re-store the first min(c, 2) symbols of a lane's range (after __syncwarp)
+__device__ __forceinline__ void fix_first2(uint32_t base_s, uint32_t e, uint32_t c, uint32_t dst, const FTab& T) {
+  SR r;
+  r.init(base_s, e);
+  const uint32_t m = c < 2 ? c : 2;
+  for (uint32_t i = 0; i < m; ++i) {
+    const uint32_t s = fone(r.peek(), T);
+    sts16(dst + 2 * i, s);
+    r.skip((s >> 16) & 0xffu);
+  }
+}
+
+// bypass: decode straight to global memory (rare; guarded by the output size)
+__device__ bool fdecode_global(SR& r, uint32_t c, uint16_t* out, uint64_t at, uint64_t nsym, const FTab& T) {
+  for (uint32_t k = 0; k < c; ++k) {
+    const uint32_t s = fone(r.peek(), T);
+    const uint32_t len = (s >> 16) & 0xffu;
+    if (!len) return false;
+    if (at + k < nsym) out[at + k] = (uint16_t)s;
+    r.skip(len);
+  }
+  return true;
 }
 
 // Re-decode a window from a new entry, walking the previous decode (entry eo,
@@ -279,13 +290,13 @@ __device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co
     if (pn >= stop) { cn = nn; xn = pn; return true; }
     if (po == pn) { cn = nn + (co - no); xn = xo; return true; }
     if (po < pn) {
-      const uint32_t l = (fone(ro.peek(), T) >> 16) & 0xffu;
+      const uint32_t l = flen(ro.peek(), T);
       if (!l) return false;
       ro.skip(l);
       po += l;
       ++no;
     } else {
-      const uint32_t l = (fone(rn.peek(), T) >> 16) & 0xffu;
+      const uint32_t l = flen(rn.peek(), T);
       if (!l) return false;
       rn.skip(l);
       pn += l;
@@ -294,7 +305,7 @@ __device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co
   }
 }
 
-// warp look-back over epoch-tagged descriptors
+// warp look-back over epoch-tagged descriptors (32 predecessors per step)
 __device__ __forceinline__ unsigned long long lookback(unsigned long long* desc, uint64_t tile, uint32_t ep) {
   const uint32_t lane = threadIdx.x & 31;
   unsigned long long excl = 0;
@@ -351,70 +362,54 @@ __device__ __forceinline__ uint4 shift_hw(uint4 A, uint4 B, uint32_t sh) {
                     __byte_perm(u3, u4, sel));
 }
 
-// 8 consecutive staged symbols starting at (signed) halfword index sidx
-__device__ __forceinline__ uint4 read8(uint32_t rows_s, int32_t sidx) {
-  const uint32_t q = rows_s + 2u * (uint32_t)(sidx & ~7);
-  return shift_hw(lds128(q), lds128(q + 16), (uint32_t)sidx & 7u);
+// Flush [P, P+C) from compact staging (stg symbol i <-> output P+i).  Whole
+// aligned chunks: two aligned 128-bit shared loads shifted by the tile's
+// (uniform) misalignment, one 128-bit global store; the two edge chunks, shared
+// with the neighbouring tiles, element by element.
+__device__ __forceinline__ void flush_compact(uint16_t* __restrict__ out, uint64_t nsym, uint64_t P, uint32_t C,
+                                              uint32_t stg_s) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t g1 = P + C;
+  const uint64_t f0 = (P + 7) & ~7ull;                   // first whole chunk
+  const uint64_t f1 = (g1 < nsym ? g1 : nsym) & ~7ull;   // end of whole chunks
+  const uint32_t sh = (uint32_t)(f0 - P) & 7u;           // uniform shift
+  if (f1 > f0) {
+    const uint32_t nfull = (uint32_t)((f1 - f0) >> 3);
+    const uint32_t s0 = (uint32_t)(f0 - P) & ~7u;        // 16B-aligned staging index of chunk 0
+    for (uint32_t ch = lane; ch < nfull; ch += 32) {
+      const uint32_t q = stg_s + 2 * (s0 + 8 * ch);
+      const uint4 A = lds128(q);
+      const uint4 v = sh ? shift_hw(A, lds128(q + 16), sh) : A;
+      *reinterpret_cast<uint4*>(out + f0 + 8ull * ch) = v;
+    }
+  }
+  // head [P, min(f0, g1)) and tail [max(f1, P), g1): at most 7 + 7 + (overlap) elements
+  const uint64_t hend = f0 < g1 ? f0 : g1;
+  const uint64_t tbeg = f1 > hend ? f1 : hend;
+  const uint32_t nh = (uint32_t)(hend - P), nt = (uint32_t)(g1 - tbeg);
+  if (lane < nh) {
+    const uint64_t g = P + lane;
+    if (g < nsym) out[g] = (uint16_t)lds16(stg_s + 2 * lane);
+  } else if (lane >= 8 && lane - 8 < nt) {
+    const uint64_t g = tbeg + (lane - 8);
+    if (g < nsym) out[g] = (uint16_t)lds16(stg_s + 2 * (uint32_t)(g - P));
+  }
 }
 
-// Gather the tile's rows into output order and flush [P, P+C) with 128-bit
-// stores.  so/sc: per-lane start (tile-local) and count arrays (so[32] = inf).
-// A chunk covers at most two lanes' rows on the common path (both rows are
-// read unconditionally to keep the warp converged); a chunk touching three or
-// more lanes (some lane with < 8 symbols) goes element by element.
-__device__ __forceinline__ void flush_rows(uint16_t* __restrict__ out, uint64_t nsym, uint64_t P, uint32_t C,
-                                           uint32_t rows_s, uint32_t row_hw, const uint32_t* so,
-                                           const uint32_t* sc) {
+// 128-bit flush of [g0, g0+len) from staging aligned to g0 (stg[0] <-> g0 & ~7)
+__device__ __forceinline__ void flush_aligned(uint16_t* __restrict__ out, uint64_t nsym, uint64_t g0, uint32_t len,
+                                              const uint16_t* stg) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint64_t a0 = P & ~7ull, g1 = P + C;
+  const uint64_t a0 = g0 & ~7ull, g1 = g0 + len;
   const uint32_t nch = (uint32_t)((g1 - a0 + 7) >> 3);
   for (uint32_t ch = lane; ch < nch; ch += 32) {
     const uint64_t ga = a0 + (uint64_t)ch * 8;
-    const int32_t x = (int32_t)(int64_t)(ga - P);  // tile-local position of the chunk (may be < 0)
-    const uint32_t xs = x < 0 ? 0u : (uint32_t)x;
-    uint32_t L = 0;  // owner of xs: largest lane with so[L] <= xs
-#pragma unroll
-    for (uint32_t step = 16; step; step >>= 1)
-      if (L + step < 32 && so[L + step] <= xs) L += step;
-    const uint32_t soL = so[L];
-    const int32_t m = (int32_t)(soL + sc[L]) - x;   // elements of the chunk inside lane L
-    uint32_t L2 = L + 1 < 32 ? L + 1 : 31;
-    const uint4 v1 = read8(rows_s, (int32_t)(L * row_hw) + (x - (int32_t)soL));
-    const uint4 v2 = read8(rows_s, (int32_t)(L2 * row_hw) + (x - (int32_t)so[L2]));
-    // halfword i comes from v1 when i < m, else from v2
-    const uint32_t mk0 = m > 1 ? 0xffffffffu : (m > 0 ? 0xffffu : 0u);
-    const uint32_t mk1 = m > 3 ? 0xffffffffu : (m > 2 ? 0xffffu : 0u);
-    const uint32_t mk2 = m > 5 ? 0xffffffffu : (m > 4 ? 0xffffu : 0u);
-    const uint32_t mk3 = m > 7 ? 0xffffffffu : (m > 6 ? 0xffffu : 0u);
-    uint4 v = make_uint4((v1.x & mk0) | (v2.x & ~mk0), (v1.y & mk1) | (v2.y & ~mk1),
-                         (v1.z & mk2) | (v2.z & ~mk2), (v1.w & mk3) | (v2.w & ~mk3));
-    const bool inside = ga >= P && ga + 8 <= g1 && ga + 8 <= nsym;
-    const int32_t need = min(8, (int32_t)C - x);  // chunk elements inside the tile (from x)
-    const bool two_ok = m >= need || (L + 1 < 32 && m + (int32_t)sc[L2] >= need);
-    if (!two_ok) {
-      // three or more lanes in one chunk: element by element
-      uint32_t h[8];
-      uint32_t Lc = L;
-#pragma unroll
-      for (uint32_t i = 0; i < 8; ++i) {
-        h[i] = 0;
-        const int32_t xi = x + (int32_t)i;
-        if (xi >= 0 && xi < (int32_t)C) {
-          while (Lc < 31 && so[Lc + 1] <= (uint32_t)xi) ++Lc;
-          h[i] = lds16(rows_s + 2 * (Lc * row_hw + ((uint32_t)xi - so[Lc])));
-        }
-      }
-      v = make_uint4(h[0] | (h[1] << 16), h[2] | (h[3] << 16), h[4] | (h[5] << 16), h[6] | (h[7] << 16));
-    }
-    if (inside) {
-      *reinterpret_cast<uint4*>(out + ga) = v;
+    if (ga >= g0 && ga + 8 <= g1 && ga + 8 <= nsym) {
+      *reinterpret_cast<uint4*>(out + ga) = *reinterpret_cast<const uint4*>(stg + ch * 8);
     } else {
-      const uint32_t hv[8] = {v.x & 0xffffu, v.x >> 16, v.y & 0xffffu, v.y >> 16,
-                              v.z & 0xffffu, v.z >> 16, v.w & 0xffffu, v.w >> 16};
-#pragma unroll
       for (uint32_t i = 0; i < 8; ++i) {
         const uint64_t gi = ga + i;
-        if (gi >= P && gi < g1 && gi < nsym) out[gi] = (uint16_t)hv[i];
+        if (gi >= g0 && gi < g1 && gi < nsym) out[gi] = stg[ch * 8 + i];
       }
     }
   }
@@ -527,14 +522,18 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
 }
 
 // One CTA processes a group of `warps` consecutive tiles per iteration (warp w
-// takes tile group*warps + w).  The group's output offset comes from one
-// decoupled look-back over group descriptors, done by warp 0 while the other
-// warps already decode into their staging rows.
+// takes tile group*warps + w).  Software pipeline, per iteration k:
+//   count the tile of group k+1 (words staged one iteration ahead),
+//   decode the tile of group k into staging,
+//   warp 0: look back for group k+1's output offset (a full iteration early),
+//   flush the tile of group k once group k's offset is published.
+// So the look-back latency never stalls the decode in steady state.
 template <int VAR>
 __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) {
   extern __shared__ __align__(16) unsigned char sm[];
-  __shared__ uint32_t s_C[32];
-  __shared__ unsigned long long s_P;
+  __shared__ uint32_t s_C[2][32];
+  __shared__ unsigned long long s_Pw[2][32];
+  __shared__ uint32_t s_arrive[2], s_gen;
   const TableHdr* hdr = static_cast<const TableHdr*>(a.table);
   if (VAR == BH_VARIANT_SYNC && !hdr->complete) {
     // the speculative windows differ from the reference's: only complete books
@@ -542,18 +541,13 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     if (blockIdx.x == 0 && threadIdx.x == 0) tag_status(a.rep, a.epoch, NEED_STAGED);
     return;
   }
+  if (threadIdx.x == 0) { s_arrive[0] = 0; s_arrive[1] = 0; s_gen = 0; }
   {
     TableLayout L(a.max_codes);
     const char* tb_ = static_cast<const char*>(a.table);
-    const uint32_t* dl = reinterpret_cast<const uint32_t*>(tb_ + L.dlut8);
-    const uint8_t* cl = reinterpret_cast<const uint8_t*>(tb_ + L.clut8);
-    uint32_t* s_dl = reinterpret_cast<uint32_t*>(sm + T_DL);
-    uint8_t* s_cl = reinterpret_cast<uint8_t*>(sm + T_CL);
-    for (uint32_t i = threadIdx.x; i < 256 * 32; i += blockDim.x) {
-      const uint32_t ent = i >> 5, ln = i & 31;
-      s_dl[i] = __ldg(dl + ent);                                   // [ent][lane]
-      s_cl[((ent >> 2) << 7) + (ln << 2) + (ent & 3)] = __ldg(cl + ent);
-    }
+    const uint2* wl = reinterpret_cast<const uint2*>(tb_ + L.wlut8);
+    uint2* s_wl = reinterpret_cast<uint2*>(sm + T_WL);
+    for (uint32_t i = threadIdx.x; i < 256 * 32; i += blockDim.x) s_wl[i] = __ldg(wl + (i >> 5));  // [ent][lane]
     const unsigned long long* gl = reinterpret_cast<const unsigned long long*>(tb_ + L.lim);
     const long long* gb = reinterpret_cast<const long long*>(tb_ + L.base);
     unsigned long long* s_lim = reinterpret_cast<unsigned long long*>(sm + T_LIM);
@@ -563,8 +557,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   FTab T;
   const uint32_t sm_s = smem_u32(sm);
-  T.dl = pin(sm_s + T_DL + 4 * lane);
-  T.cl = pin(sm_s + T_CL + 4 * lane);
+  T.wl = sm_s + T_WL + 8 * lane;
   T.lim = sm_s + T_LIM;
   T.base = sm_s + T_BASE;
   T.t = table_view(a.table, a.max_codes, hdr->ncodes);
@@ -574,79 +567,166 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
   unsigned char* pw = sm + a.tables_bytes + (size_t)wib * a.per_warp_bytes;
   uint32_t* const wbase = reinterpret_cast<uint32_t*>(pw);
   const uint32_t wbase_s = smem_u32(pw);
-  const uint32_t rows_s = wbase_s + 8 * a.wpb;                 // 32 rows of row_words words
-  uint32_t* s_o = reinterpret_cast<uint32_t*>(pw + 8 * (size_t)a.wpb + 128 * (size_t)a.row_words);
-  uint32_t* s_c = s_o + 33;
-  const uint32_t row_hw = 2 * a.row_words;                     // row stride in symbols
-  const uint32_t my_row = rows_s + 4 * a.row_words * lane;
+  const uint32_t stg_s = wbase_s + 12 * a.wpb;  // three word buffers, then staging
+  const uint16_t* stg = reinterpret_cast<const uint16_t*>(pw + 12 * (size_t)a.wpb);
   const uint32_t W = a.warps;
   const uint64_t ngroups = (a.nseq + W - 1) / W;
+  const uint64_t G = gridDim.x;
   const uint32_t ep = a.epoch;
   bool bad = false;
 
-  uint64_t grp = blockIdx.x;
-  uint64_t wbit_cur = 0, wbit_next = 0;
-  uint32_t cur = 0;
-  if (grp * W + wib < a.nseq) wbit_cur = stage_words(a, grp * W + wib, wbase);
-  cp_commit();
-  for (; grp < ngroups; grp += gridDim.x) {
-    const uint64_t tile = grp * W + wib;
-    const uint64_t ntile = (grp + gridDim.x) * W + wib;
-    if (ntile < a.nseq) wbit_next = stage_words(a, ntile, wbase + (cur ^ 1) * a.wpb);
-    cp_commit();
-    cp_wait<1>();
-    __syncwarp();
-    const uint32_t base_s = wbase_s + cur * a.wpb * 4;
-    const uint64_t wb0 = wbit_cur;
-    const bool have = tile < a.nseq;
-    uint32_t nsl = 0, e = 0, c = 0;
-    if (have) {
-      nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
-      tile_counts<VAR>(a, T, tile, base_s, wb0, nsl, e, c, bad);
+  // warp 0: wait for every warp's count of group `g` (arrivals are counted per
+  // group parity: a fast warp can run at most one group ahead), look back,
+  // publish per-warp output offsets into s_Pw[par].
+  auto publish = [&](uint64_t g, uint32_t par, uint32_t arrivals, uint32_t gen) {
+    if (lane == 0) {
+      while (*(volatile uint32_t*)&s_arrive[par] < arrivals) __nanosleep(20);
     }
-    uint32_t incl = c;
+    __syncwarp();
+    __threadfence_block();
+    const uint32_t v = lane < W ? *(volatile uint32_t*)&s_C[par][lane] : 0u;
+    uint32_t pre = v;
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, pre, off);
+      if ((int)lane >= off) pre += y;
+    }
+    const unsigned long long A = __shfl_sync(0xffffffffu, pre, 31);
+    unsigned long long Pg = 0;
+    if (g == 0) {
+      if (lane == 0) st_release(a.cnt_desc, mkdesc(ep, D_INC, A));
+    } else {
+      if (lane == 0) st_release(a.cnt_desc + g, mkdesc(ep, D_AGG, A));
+      Pg = lookback(a.cnt_desc, g, ep);
+      if (lane == 0) st_release(a.cnt_desc + g, mkdesc(ep, D_INC, Pg + A));
+    }
+    if (lane < W) s_Pw[par][lane] = Pg + (pre - v);
+    if (lane == 0 && g == ngroups - 1) {
+      a.rep->total_symbols = Pg + A;
+      if (Pg + A != a.nsym) tag_status(a.rep, ep, VAR == BH_VARIANT_GAP ? BH_BADGAP : BH_TRUNCATED);
+    }
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) *(volatile uint32_t*)&s_gen = gen;
+  };
+
+  // per-tile state kept across the pipeline
+  struct TileState { uint32_t e, c, o, C, nsl; uint64_t wb0; };
+  auto count_tile = [&](uint64_t tile, uint32_t buf, uint64_t wb0, uint32_t par) -> TileState {
+    TileState s;
+    s.wb0 = wb0;
+    s.e = 0;
+    s.c = 0;
+    s.nsl = 0;
+    if (tile < a.nseq) {
+      s.nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
+      tile_counts<VAR>(a, T, tile, wbase_s + 4 * a.wpb * buf, wb0, s.nsl, s.e, s.c, bad);
+    }
+    uint32_t incl = s.c;
     for (int off = 1; off < 32; off <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
       if ((int)lane >= off) incl += y;
     }
-    const uint32_t C = __shfl_sync(0xffffffffu, incl, 31);
-    const uint32_t o = incl - c;
-    s_o[lane] = o;
-    s_c[lane] = c;
-    if (lane == 0) { s_C[wib] = C; s_o[32] = 0xffffffffu; }
-    __syncthreads();
-    if (wib == 0) {
-      const uint32_t v = lane < W ? s_C[lane] : 0u;
-      const unsigned long long A = warp_sum((unsigned long long)v);
-      unsigned long long Pg = 0;
-      if (grp == 0) {
-        if (lane == 0) st_release(a.cnt_desc, mkdesc(ep, D_INC, A));
-      } else {
-        if (lane == 0) st_release(a.cnt_desc + grp, mkdesc(ep, D_AGG, A));
-        Pg = lookback(a.cnt_desc, grp, ep);
-        if (lane == 0) st_release(a.cnt_desc + grp, mkdesc(ep, D_INC, Pg + A));
-      }
-      if (lane == 0) {
-        s_P = Pg;
-        if (grp == ngroups - 1) {
-          a.rep->total_symbols = Pg + A;
-          if (Pg + A != a.nsym) tag_status(a.rep, ep, VAR == BH_VARIANT_GAP ? BH_BADGAP : BH_TRUNCATED);
-        }
-      }
+    s.C = __shfl_sync(0xffffffffu, incl, 31);
+    s.o = incl - s.c;
+    if (lane == 0) {
+      s_C[par][wib] = s.C;
+      __threadfence_block();
+      atomicAdd(&s_arrive[par], 1u);
     }
-    if (have && c) {
-      SR r;
-      r.init(base_s, e);
-      if (!fdecode_row(r, c, my_row, base_s, T)) bad = true;
-    }
-    __syncthreads();  // s_P published; rows complete
-    uint32_t before = lane < wib ? s_C[lane] : 0u;
-    for (int off = 16; off > 0; off >>= 1) before += __shfl_xor_sync(0xffffffffu, before, off);
-    const unsigned long long P = s_P + before;
-    if (have) flush_rows(a.out, a.nsym, P, C, rows_s, row_hw, s_o, s_c);
+    return s;
+  };
+
+  const uint64_t g0 = blockIdx.x;
+  if (g0 >= ngroups) return;
+  // prologue: stage groups g0 and g0+G, count g0, publish its offsets
+  uint64_t wb_cur = 0, wb_next = 0, wb_nn = 0;
+  if (g0 * W + wib < a.nseq) wb_cur = stage_words(a, g0 * W + wib, wbase);
+  cp_commit();
+  if ((g0 + G) * W + wib < a.nseq) wb_next = stage_words(a, (g0 + G) * W + wib, wbase + a.wpb);
+  cp_commit();
+  cp_wait<1>();
+  __syncwarp();
+  TileState cur = count_tile(g0 * W + wib, 0, wb_cur, 0);
+  if (wib == 0) publish(g0, 0, W, 1);  // group #0 of this CTA: parity 0, 1st occurrence
+
+  uint32_t k = 0, bcur = 0, bnext = 1, bnn = 2;
+  for (uint64_t g = g0; g < ngroups; g += G, ++k) {
+    const uint32_t par = k & 1;
+    const uint64_t gn = g + G, gnn = g + 2 * G;
+    const uint64_t tile = g * W + wib;
+    if (gnn * W + wib < a.nseq) wb_nn = stage_words(a, gnn * W + wib, wbase + bnn * a.wpb);
+    cp_commit();
+    cp_wait<1>();  // buffers of groups g and g+G have landed
     __syncwarp();
-    cur ^= 1;
-    wbit_cur = wbit_next;
+    // count the next group's tile
+    TileState nxt = cur;
+    if (gn < ngroups) nxt = count_tile(gn * W + wib, bnext, wb_next, par ^ 1);
+    // decode this group's tile into staging
+    const uint32_t base_s = wbase_s + 4 * a.wpb * bcur;
+    const bool have = tile < a.nseq;
+    const bool fits = cur.C + 16 <= a.cap;
+    if (have && fits && cur.c) {
+      SR r;
+      r.init(base_s, cur.e);
+      if (!fdecode(r, cur.c, stg_s + 2 * cur.o, T)) bad = true;
+    }
+    __syncwarp();
+    // warp 0 looks back for the next group (needed one iteration from now)
+    if (wib == 0 && gn < ngroups) publish(gn, par ^ 1, ((k + 1) / 2 + 1) * W, k + 2);  // group #k+1
+    // flush once this group's offsets are published
+    if (lane == 0) {
+      while (*(volatile uint32_t*)&s_gen < k + 1) __nanosleep(20);
+    }
+    __syncwarp();
+    __threadfence_block();
+    const unsigned long long P = *(volatile unsigned long long*)&s_Pw[par][wib];
+    if (have && fits) {
+      flush_compact(a.out, a.nsym, P, cur.C, stg_s);
+    } else if (have) {
+      // reference rounds (staging.py:123-146) with capacity cap - 8
+      const bool active = lane < cur.nsl;
+      const uint32_t capw = a.cap - 8;
+      const uint32_t endl = cur.o + cur.c;
+      uint32_t si = 0;
+      while (si < cur.C) {
+        const uint32_t window = si + capw;
+        const unsigned mj = __ballot_sync(0xffffffffu, active && endl > si);
+        const uint32_t jl = __ffs(mj) - 1;
+        const unsigned mk = __ballot_sync(0xffffffffu, active && lane >= jl && endl > window);
+        const uint32_t kl = mk ? __ffs(mk) - 1 : cur.nsl;
+        if (kl == jl) {
+          if (lane == jl) {
+            SR r;
+            r.init(base_s, cur.e);
+            if (!fdecode_global(r, cur.c, a.out, P + cur.o, a.nsym, T)) bad = true;
+          }
+          si = __shfl_sync(0xffffffffu, endl, jl);
+          continue;
+        }
+        const uint32_t temp_end = kl < cur.nsl ? __shfl_sync(0xffffffffu, cur.o, kl & 31) : cur.C;
+        const uint64_t g0w = P + si;
+        const uint64_t gbase = g0w & ~7ull;
+        const bool mine = lane >= jl && lane < kl && cur.c;
+        const uint32_t d = stg_s + 2 * (uint32_t)(P + cur.o - gbase);
+        if (mine) {
+          SR r;
+          r.init(base_s, cur.e);
+          if (!fdecode(r, cur.c, d, T)) bad = true;
+        }
+        __syncwarp();
+        flush_aligned(a.out, a.nsym, g0w, temp_end - si, stg);
+        __syncwarp();
+        si = temp_end;
+      }
+    }
+    __syncwarp();
+    cur = nxt;
+    wb_cur = wb_next;
+    wb_next = wb_nn;
+    const uint32_t bt = bcur;
+    bcur = bnext;
+    bnext = bnn;
+    bnn = bt;
   }
   cp_wait<0>();
   if (__any_sync(0xffffffffu, bad) && lane == 0) tag_status(a.rep, ep, BH_INVALID);
@@ -684,18 +764,27 @@ int env_int(const char* name, int dflt) {
 }
 
 struct FusedCfg {
-  uint32_t warps, row_words, wpb, per_warp, tables, smem;
+  uint32_t warps, cap, wpb, per_warp, tables, smem;
 };
 
 FusedCfg fused_cfg(const bh_stream* s) {
   FusedCfg c;
   const uint32_t seq_bits = s->subseq_bits * s->subseqs_per_seq;
-  c.wpb = ((seq_bits + 31) / 32 + 3 + HALO_WORDS + 3) & ~3u;
-  // a slot counts codewords starting in [entry, stop): at most subseq_bits + 31
-  const uint32_t max_c = s->subseq_bits + 31;
-  c.row_words = ((max_c + 1) / 2) | 1u;  // odd: lane rows fall in distinct banks
+  // words one tile can stage: its span (+1 for a straddle), the 16-byte
+  // alignment of the first word (+3), the halo, rounded up to 16 bytes
+  c.wpb = ((seq_bits + 31) / 32 + 1 + 3 + HALO_WORDS + 3) & ~3u;
+  // staging sized from the header's compression ratio (no device round trip):
+  // a tile emits about seq_bits * symbols / total_bits symbols; a tile above
+  // the capacity takes the reference's rounds, so any value is correct
+  const double per_bit = s->total_bits ? (double)s->symbol_count / (double)s->total_bits : 1.0;
+  uint32_t cap = (uint32_t)(seq_bits * per_bit * 1.12) + 96;
+  if (env_int("BH_FUSED_CAP", 0)) cap = (uint32_t)env_int("BH_FUSED_CAP", 0);
+  const uint32_t cmax = s->subseqs_per_seq * (s->subseq_bits + 31) + 16;
+  if (cap > cmax) cap = cmax;
+  if (cap < 64) cap = 64;
+  c.cap = (cap + 7) & ~7u;
   c.tables = (uint32_t)align16(T_END);
-  c.per_warp = (uint32_t)align16(8 * (size_t)c.wpb + 128 * (size_t)c.row_words + 4 * 66);
+  c.per_warp = (uint32_t)align16(12 * (size_t)c.wpb + 2 * (size_t)c.cap + 32);
   int w = env_int("BH_FUSED_WARPS", 0);
   if (w <= 0) {
     w = (int)((220 * 1024 - c.tables) / c.per_warp);
@@ -714,7 +803,7 @@ extern "C" int bh_fused_supported(const bh_stream* s, int variant) {
   if (variant != BH_VARIANT_GAP && variant != BH_VARIANT_SYNC) return 0;
   if (s->subseqs_per_seq > 32 || s->subseqs_per_seq == 0) return 0;
   const uint64_t seq_bits = (uint64_t)s->subseq_bits * s->subseqs_per_seq;
-  if (seq_bits > 16384 || s->subseq_bits > 512 || s->total_bits >= (1ull << 36) || s->symbol_count >= (1ull << 36)) return 0;
+  if (seq_bits > 16384 || s->total_bits >= (1ull << 36) || s->symbol_count >= (1ull << 36)) return 0;
   if (variant == BH_VARIANT_GAP && !s->gap_dev) return 0;
   FusedCfg c = fused_cfg(s);
   return c.smem <= 227 * 1024 ? 1 : 0;
@@ -754,7 +843,7 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.rep = static_cast<DevReport*>(report_dev);
   a.epoch = next_epoch();
   a.wpb = cfg.wpb;
-  a.row_words = cfg.row_words;
+  a.cap = cfg.cap;
   a.warps = cfg.warps;
   a.per_warp_bytes = cfg.per_warp;
   a.tables_bytes = cfg.tables;
