@@ -1,0 +1,74 @@
+"""Multi-GPU sharding of the decode path.
+
+Decoding shards with no collective on the data path:
+
+* a batch of independent fields (the multi-field config) is spread over ranks
+  by longest-processing-time on payload bits, every rank decoding its own
+  fields into its own output;
+* one long stream is cut at sequence boundaries, so every shard's entry bits
+  are known (boundary + gap byte) and shards are independent; the only
+  exchange is the per-shard symbol totals (8 bytes per rank) that place each
+  shard's output, done off the timed path.
+
+Timing over ranks is the max of the per-rank device times (``max_over_ranks``).
+"""
+
+from __future__ import annotations
+
+import heapq
+
+
+def lpt_assign(sizes, world: int) -> list[list[int]]:
+    """Indices of `sizes` per rank, greedy longest-processing-time first."""
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    heap = [(0, r) for r in range(world)]
+    out: list[list[int]] = [[] for _ in range(world)]
+    for i in sorted(range(len(sizes)), key=lambda i: (-sizes[i], i)):
+        load, r = heapq.heappop(heap)
+        out[r].append(i)
+        heapq.heappush(heap, (load + sizes[i], r))
+    for lst in out:
+        lst.sort()
+    return out
+
+
+def sequence_ranges(num_seqs: int, world: int) -> list[tuple[int, int]]:
+    """Contiguous, sequence-aligned [q0, q1) per rank (sizes differ by <= 1)."""
+    base, extra = divmod(num_seqs, world)
+    out, q = [], 0
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        out.append((q, q + n))
+        q += n
+    return out
+
+
+def shard_offsets(totals) -> list[int]:
+    """Exclusive prefix of per-shard symbol totals (where each shard's output starts)."""
+    acc, out = 0, []
+    for t in totals:
+        out.append(acc)
+        acc += int(t)
+    return out
+
+
+def gather_totals(total: int, group=None) -> list[int]:
+    """All ranks' symbol totals (a tiny collective, outside the timed region)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([int(total)], dtype=torch.int64, device=dev)
+    parts = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(parts, t, group=group)
+    return [int(p.item()) for p in parts]
+
+
+def max_over_ranks(value: float, group=None) -> float:
+    import torch
+    import torch.distributed as dist
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    return float(t.item())

@@ -250,6 +250,21 @@ def main():
     record("bad_gap", cg, book_for(cg, 16), ph.DEFAULT_LAYOUT, out=out, gap_edit=edit)
     record("bad_header_gap", cg, book_for(cg, 16), ph.DEFAULT_LAYOUT, out=out, header_delta=-3)
 
+    # HUF2 containers written by the reference (byte-compatibility fixtures)
+    cdir = HERE / "containers"
+    cdir.mkdir(exist_ok=True)
+    for name in ("zipf_16_3_5_w8", "zipf_32_4_32_w16", "gauss_1m_head", "empty", "single_symbol",
+                 "trailing", "deep31", "zipf_8_1_32_w8"):
+        z = np.load(out / f"{name}.npz")
+        lens = z["lens"]
+        nz = np.nonzero(lens)[0]
+        book = ph.canonize({int(s): int(lens[s]) for s in nz}, symbol_width=int(z["symbol_width"]))
+        lay = ph.LayoutConfig(int(z["unit_bits"]), int(z["ups"]), int(z["sps"]))
+        st = ph.EncodedStream(layout=lay, units=z["units"].astype(np.uint32), total_bits=int(z["total_bits"]),
+                              symbol_count=int(z["symbol_count"]), codebook=book,
+                              gap=z["gap"] if int(z["has_gap"]) else None)
+        ph.write_container(st, cdir / f"{name}.huf2")
+
     digests = {}
     for key in ("1m", "hurricane"):
         spec = FIELDS[key]
