@@ -44,7 +44,12 @@
 namespace bh {
 
 constexpr int HALO_WORDS = 8;
-constexpr int FUSED_MAX_THREADS = 1024;
+// interleave the next tile's count with the current decode (gap variant):
+// measured slower on B200 (later count arrivals stall the pipelined look-back)
+#ifndef BH_INTERLEAVE_COUNT
+#define BH_INTERLEAVE_COUNT 0
+#endif
+constexpr int FUSED_MAX_THREADS = 768;  // <= 24 warps: up to 85 registers per thread
 constexpr uint32_t NEED_STAGED = 9;  // BH_NEED_STAGED
 
 // descriptor: [63:38] epoch (26 bits) | [37:36] flags | [35:0] value
@@ -129,26 +134,40 @@ __device__ __forceinline__ uint32_t pin(uint32_t v) {
   return v;
 }
 
-// Bit reader over a tile's staged words; positions are tile-relative bits.
+// predicated shared load (no branch): returns `v` unchanged when !p
+__device__ __forceinline__ uint32_t lds32_if(uint32_t a, uint32_t p, uint32_t v) {
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.u32 %0, [%1];\n\t}"
+               : "+r"(v) : "r"(a), "r"(p) : "memory");
+  return v;
+}
+
+// Bit reader over a tile's staged words (tile-relative bit positions): the
+// current and next word plus one prefetched word, and a bit offset.  peek is
+// one funnel shift; skip advances by at most one word with selects and a
+// predicated load of the word after next -- no branch, and the loaded word is
+// only needed one advance later, so shared-memory latency stays off the
+// decode chain.
 struct SR {
-  uint64_t buf;
-  uint32_t av;
-  uint32_t wa;  // shared address of the next word to load
+  uint32_t w0, w1, w2;  // MSB-first words at the cursor
+  uint32_t off;         // bit offset into w0 (0..31)
+  uint32_t wa;          // shared address of the word after w2
   __device__ __forceinline__ void init(uint32_t base_s, uint32_t rel) {
     const uint32_t a = base_s + ((rel >> 5) << 2);
-    buf = (((uint64_t)lds32(a) << 32) | lds32(a + 4)) << (rel & 31);
-    av = 64 - (rel & 31);
-    wa = a + 8;
+    w0 = lds32(a);
+    w1 = lds32(a + 4);
+    w2 = lds32(a + 8);
+    off = rel & 31;
+    wa = a + 12;
   }
-  __device__ __forceinline__ uint32_t peek() const { return (uint32_t)(buf >> 32); }
-  __device__ __forceinline__ void skip(uint32_t n) {
-    buf <<= n;
-    av -= n;
-    if (av < 32) {
-      buf |= (uint64_t)lds32(wa) << (32 - av);
-      wa += 4;
-      av += 32;
-    }
+  __device__ __forceinline__ uint32_t peek() const { return __funnelshift_l(w1, w0, off); }
+  __device__ __forceinline__ void skip(uint32_t n) {  // n <= 32
+    const uint32_t t = off + n;
+    const uint32_t adv = t >> 5;
+    w0 = adv ? w1 : w0;
+    w1 = adv ? w2 : w1;
+    w2 = lds32_if(wa, adv, w2);
+    wa += adv << 2;
+    off = t & 31;
   }
 };
 
@@ -415,6 +434,23 @@ __device__ __forceinline__ void flush_aligned(uint16_t* __restrict__ out, uint64
   }
 }
 
+// GAP: tile-relative entry and stop of this lane's slot (gap_decoder.py:24-53)
+__device__ __forceinline__ void gap_window(const FusedArgs& a, uint64_t tile, uint64_t wb0, uint32_t nsl,
+                                           uint32_t& e, uint32_t& stop) {
+  const uint32_t lane = threadIdx.x & 31;
+  const bool active = lane < nsl;
+  const uint64_t j = tile * a.sps + lane;
+  const uint32_t b = (uint32_t)(j * a.sb - wb0);
+  const uint32_t tbr = (uint32_t)min(a.tb - wb0, (uint64_t)0xffffffffu);
+  const uint32_t g = active ? a.gap[j] : 0u;
+  uint32_t gn = __shfl_down_sync(0xffffffffu, g, 1);
+  if (lane == nsl - 1) gn = (j + 1 < a.nsub) ? a.gap[j + 1] : 0u;
+  e = b + g;
+  stop = (j + 1 < a.nsub) ? b + a.sb + gn : tbr;
+  if (stop > tbr) stop = tbr;
+  if (!active) stop = e;
+}
+
 // Entries and counts of one tile (lane = subsequence); positions are relative
 // to the tile buffer's first bit `wb0`.  GAP: boundary + gap byte; SYNC:
 // intra-sequence chain rounds plus the seam seed from the predecessor tile's
@@ -521,6 +557,56 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
   if (!active) c = 0;
 }
 
+// GAP variant: the count chain of the next tile and the decode chain of the
+// current tile are independent, so one loop advances both (two dependent
+// chains per lane hide each other's shared-memory and ALU latency).
+// Count: codewords starting in [pc, stopc); decode: kd symbols to `dst`.
+__device__ __forceinline__ bool count_decode2(SR& rc, uint32_t& pc, uint32_t stopc, uint32_t& nc, SR& rd,
+                                              uint32_t kd_, uint32_t dst, const FTab& T) {
+  const uint32_t wl = pin(T.wl);
+  bool ok = true;
+  int32_t kd = (int32_t)kd_;
+  while (pc < stopc || kd > 0) {
+    if (pc < stopc) {
+      const uint32_t win = rc.peek();
+      const uint32_t y = lds32(wl + 4 + ((win >> 24) << 8));
+      uint32_t b;
+      if (y && pc + 8 <= stopc) {
+        nc += (y >> 24) & 15u;
+        b = (y >> 28) + 1;
+      } else {
+        b = y ? ((y >> 21) & 7u) + 1 : (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t) >> 16) & 0xffu;
+        nc += 1;
+        if (!b) { ok = false; b = stopc - pc; }  // unmatched pattern: stop this window
+      }
+      rc.skip(b < 32 ? b : 32);
+      pc += b;
+    }
+    if (kd > 0) {
+      const uint32_t win = rd.peek();
+      const uint2 w = lds64(wl + ((win >> 24) << 8));
+      if (w.y) {
+        const uint32_t n = (w.y >> 16) & 3u;
+        sts16(dst, w.x);
+        if (n > 1 && kd > 1) sts16(dst + 2, w.x >> 16);
+        if (n > 2 && kd > 2) sts16(dst + 4, w.y);
+        dst += n << 1;
+        kd -= (int32_t)n;
+        rd.skip(((w.y >> 18) & 7u) + 1);
+      } else {
+        const uint32_t e = fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t);
+        const uint32_t len = (e >> 16) & 0xffu;
+        if (!len) { ok = false; kd = 0; continue; }
+        sts16(dst, e);
+        dst += 2;
+        kd -= 1;
+        rd.skip(len);
+      }
+    }
+  }
+  return ok;
+}
+
 // One CTA processes a group of `warps` consecutive tiles per iteration (warp w
 // takes tile group*warps + w).  Software pipeline, per iteration k:
 //   count the tile of group k+1 (words staged one iteration ahead),
@@ -611,6 +697,20 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
 
   // per-tile state kept across the pipeline
   struct TileState { uint32_t e, c, o, C, nsl; uint64_t wb0; };
+  auto finish_count = [&](TileState& s, uint32_t par) {
+    uint32_t incl = s.c;
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      if ((int)lane >= off) incl += y;
+    }
+    s.C = __shfl_sync(0xffffffffu, incl, 31);
+    s.o = incl - s.c;
+    if (lane == 0) {
+      s_C[par][wib] = s.C;
+      __threadfence_block();
+      atomicAdd(&s_arrive[par], 1u);
+    }
+  };
   auto count_tile = [&](uint64_t tile, uint32_t buf, uint64_t wb0, uint32_t par) -> TileState {
     TileState s;
     s.wb0 = wb0;
@@ -658,21 +758,46 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     cp_commit();
     cp_wait<1>();  // buffers of groups g and g+G have landed
     __syncwarp();
-    // count the next group's tile
-    TileState nxt = cur;
-    if (gn < ngroups) nxt = count_tile(gn * W + wib, bnext, wb_next, par ^ 1);
-    // decode this group's tile into staging
     const uint32_t base_s = wbase_s + 4 * a.wpb * bcur;
     const bool have = tile < a.nseq;
     const bool fits = cur.C + 16 <= a.cap;
-    if (have && fits && cur.c) {
-      SR r;
-      r.init(base_s, cur.e);
-      if (!fdecode(r, cur.c, stg_s + 2 * cur.o, T)) bad = true;
+    TileState nxt = cur;
+    if (VAR == BH_VARIANT_GAP && BH_INTERLEAVE_COUNT) {
+      // count the next group's tile while decoding this group's tile
+      const uint64_t ntile = gn * W + wib;
+      const bool nhave = gn < ngroups && ntile < a.nseq;
+      uint32_t nsl = 0, ne = 0, nstop = 0;
+      if (nhave) {
+        nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - ntile * a.sps);
+        gap_window(a, ntile, wb_next, nsl, ne, nstop);
+      }
+      SR rc, rd;
+      uint32_t pc = ne, nc = 0;
+      if (nhave && lane < nsl && ne < nstop) rc.init(wbase_s + 4 * a.wpb * bnext, ne);
+      else nstop = pc;  // nothing to count
+      const uint32_t kd = (have && fits && cur.c) ? cur.c : 0u;
+      if (kd) rd.init(base_s, cur.e);
+      if (!count_decode2(rc, pc, nstop, nc, rd, kd, stg_s + 2 * cur.o, T)) bad = true;
+      if (gn < ngroups) {
+        nxt.wb0 = wb_next;
+        nxt.e = ne;
+        nxt.c = (nhave && lane < nsl) ? nc : 0u;
+        nxt.nsl = nsl;
+        finish_count(nxt, par ^ 1);
+      }
+    } else {
+      // count the next group's tile, then decode this group's tile
+      if (gn < ngroups) nxt = count_tile(gn * W + wib, bnext, wb_next, par ^ 1);
+      if (have && fits && cur.c) {
+        SR r;
+        r.init(base_s, cur.e);
+        if (!fdecode(r, cur.c, stg_s + 2 * cur.o, T)) bad = true;
+      }
     }
     __syncwarp();
-    // warp 0 looks back for the next group (needed one iteration from now)
-    if (wib == 0 && gn < ngroups) publish(gn, par ^ 1, ((k + 1) / 2 + 1) * W, k + 2);  // group #k+1
+    // one warp (rotating, so no warp carries every look-back) publishes the
+    // next group's offsets -- needed one iteration from now
+    if (wib == (k + 1) % W && gn < ngroups) publish(gn, par ^ 1, ((k + 1) / 2 + 1) * W, k + 2);  // group #k+1
     // flush once this group's offsets are published
     if (lane == 0) {
       while (*(volatile uint32_t*)&s_gen < k + 1) __nanosleep(20);
@@ -788,9 +913,10 @@ FusedCfg fused_cfg(const bh_stream* s) {
   int w = env_int("BH_FUSED_WARPS", 0);
   if (w <= 0) {
     w = (int)((220 * 1024 - c.tables) / c.per_warp);
-    if (w > 32) w = 32;
+    if (w > 24) w = 24;
     if (w < 1) w = 1;
   }
+  if (w > 24) w = 24;
   c.warps = (uint32_t)w;
   c.smem = c.tables + c.warps * c.per_warp;
   return c;
