@@ -86,8 +86,10 @@ struct FusedArgs {
 };
 
 // shared-memory table layout inside the CTA (bytes)
-constexpr uint32_t T_WL = 0;                      // uint2 [256][32] replicated wlut8
-constexpr uint32_t T_LIM = T_WL + 256 * 32 * 8;   // u64 [33]
+// wlut8 is replicated 16 times ([entry][16] uint2): an LDS.64 is served per
+// half-warp, so lane l reading replica l%16 never conflicts (32 KB, not 64).
+constexpr uint32_t T_WL = 0;                      // uint2 [256][16] replicated wlut8
+constexpr uint32_t T_LIM = T_WL + 256 * 16 * 8;   // u64 [33]
 constexpr uint32_t T_BASE = T_LIM + 33 * 8;       // i64 [33]
 constexpr uint32_t T_END = T_BASE + 33 * 8;
 
@@ -200,13 +202,13 @@ __device__ __noinline__ uint32_t fslow(uint32_t win, const uint32_t lim_s, const
 
 // one codeword: sym | len<<16 (0 = no codeword matches)
 __device__ __forceinline__ uint32_t fone(uint32_t win, const FTab& T) {
-  const uint2 w = lds64(T.wl + ((win >> 24) << 8));
+  const uint2 w = lds64(T.wl + ((win >> 24) << 7));
   if (w.y) return (w.x & 0xffffu) | ((((w.y >> 21) & 7u) + 1) << 16);
   return fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t);
 }
 
 __device__ __forceinline__ uint32_t flen(uint32_t win, const FTab& T) {
-  const uint32_t y = lds32(T.wl + ((win >> 24) << 8) + 4);
+  const uint32_t y = lds32(T.wl + ((win >> 24) << 7) + 4);
   if (y) return ((y >> 21) & 7u) + 1;
   return (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t) >> 16) & 0xffu;
 }
@@ -216,7 +218,7 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
   const uint32_t wy = pin(T.wl + 4);
   while (pos + 8 <= stop) {  // every whole codeword of the next 8 bits starts before stop
     const uint32_t win = r.peek();
-    const uint32_t y = lds32(wy + ((win >> 24) << 8));
+    const uint32_t y = lds32(wy + ((win >> 24) << 7));
     if (!y) break;
     const uint32_t b = (y >> 28) + 1;
     n += (y >> 24) & 15u;
@@ -232,7 +234,7 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
     if (pos + 8 <= stop) {  // back to the multi-codeword path after a long code
       while (pos + 8 <= stop) {
         const uint32_t win = r.peek();
-        const uint32_t y = lds32(wy + ((win >> 24) << 8));
+        const uint32_t y = lds32(wy + ((win >> 24) << 7));
         if (!y) break;
         const uint32_t b = (y >> 28) + 1;
         n += (y >> 24) & 15u;
@@ -251,7 +253,7 @@ __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const F
   int32_t k = (int32_t)c;
   while (k > 0) {
     const uint32_t win = r.peek();
-    const uint2 w = lds64(wl + ((win >> 24) << 8));
+    const uint2 w = lds64(wl + ((win >> 24) << 7));
     if (w.y) {
       const uint32_t n = (w.y >> 16) & 3u;
       sts16(dst, w.x);
@@ -569,7 +571,7 @@ __device__ __forceinline__ bool count_decode2(SR& rc, uint32_t& pc, uint32_t sto
   while (pc < stopc || kd > 0) {
     if (pc < stopc) {
       const uint32_t win = rc.peek();
-      const uint32_t y = lds32(wl + 4 + ((win >> 24) << 8));
+      const uint32_t y = lds32(wl + 4 + ((win >> 24) << 7));
       uint32_t b;
       if (y && pc + 8 <= stopc) {
         nc += (y >> 24) & 15u;
@@ -584,7 +586,7 @@ __device__ __forceinline__ bool count_decode2(SR& rc, uint32_t& pc, uint32_t sto
     }
     if (kd > 0) {
       const uint32_t win = rd.peek();
-      const uint2 w = lds64(wl + ((win >> 24) << 8));
+      const uint2 w = lds64(wl + ((win >> 24) << 7));
       if (w.y) {
         const uint32_t n = (w.y >> 16) & 3u;
         sts16(dst, w.x);
@@ -633,7 +635,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     const char* tb_ = static_cast<const char*>(a.table);
     const uint2* wl = reinterpret_cast<const uint2*>(tb_ + L.wlut8);
     uint2* s_wl = reinterpret_cast<uint2*>(sm + T_WL);
-    for (uint32_t i = threadIdx.x; i < 256 * 32; i += blockDim.x) s_wl[i] = __ldg(wl + (i >> 5));  // [ent][lane]
+    for (uint32_t i = threadIdx.x; i < 256 * 16; i += blockDim.x) s_wl[i] = __ldg(wl + (i >> 4));  // [ent][replica]
     const unsigned long long* gl = reinterpret_cast<const unsigned long long*>(tb_ + L.lim);
     const long long* gb = reinterpret_cast<const long long*>(tb_ + L.base);
     unsigned long long* s_lim = reinterpret_cast<unsigned long long*>(sm + T_LIM);
@@ -643,7 +645,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   FTab T;
   const uint32_t sm_s = smem_u32(sm);
-  T.wl = sm_s + T_WL + 8 * lane;
+  T.wl = sm_s + T_WL + 8 * (lane & 15);
   T.lim = sm_s + T_LIM;
   T.base = sm_s + T_BASE;
   T.t = table_view(a.table, a.max_codes, hdr->ncodes);
