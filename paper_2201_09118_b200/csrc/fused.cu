@@ -417,6 +417,36 @@ __device__ __forceinline__ void flush_compact(uint16_t* __restrict__ out, uint64
   }
 }
 
+// Flush [P, P+C) from staging aligned to the output: stg symbol i <-> output
+// (P & ~7) + i.  Whole chunks: one aligned 128-bit shared load and one
+// 128-bit global store; the edge chunks shared with neighbouring tiles go
+// element by element.
+__device__ __forceinline__ void flush_aligned_stg(uint16_t* __restrict__ out, uint64_t nsym, uint64_t P, uint32_t C,
+                                                  uint32_t stg_s) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t a0 = P & ~7ull, g1 = P + C;
+  const uint64_t f0 = (P + 7) & ~7ull;                   // first whole chunk
+  const uint64_t f1 = (g1 < nsym ? g1 : nsym) & ~7ull;   // end of whole chunks
+  if (f1 > f0) {
+    const uint32_t c0 = (uint32_t)(f0 - a0) >> 3;
+    const uint32_t nfull = (uint32_t)((f1 - f0) >> 3);
+    for (uint32_t ch = lane; ch < nfull; ch += 32) {
+      const uint4 v = lds128(stg_s + 16 * (c0 + ch));
+      *reinterpret_cast<uint4*>(out + f0 + 8ull * ch) = v;
+    }
+  }
+  const uint64_t hend = f0 < g1 ? f0 : g1;
+  const uint64_t tbeg = f1 > hend ? f1 : hend;
+  const uint32_t nh = (uint32_t)(hend - P), nt = (uint32_t)(g1 - tbeg);
+  if (lane < nh) {
+    const uint64_t g = P + lane;
+    if (g < nsym) out[g] = (uint16_t)lds16(stg_s + 2 * (uint32_t)(g - a0));
+  } else if (lane >= 8 && lane - 8 < nt) {
+    const uint64_t g = tbeg + (lane - 8);
+    if (g < nsym) out[g] = (uint16_t)lds16(stg_s + 2 * (uint32_t)(g - a0));
+  }
+}
+
 // 128-bit flush of [g0, g0+len) from staging aligned to g0 (stg[0] <-> g0 & ~7)
 __device__ __forceinline__ void flush_aligned(uint16_t* __restrict__ out, uint64_t nsym, uint64_t g0, uint32_t len,
                                               const uint16_t* stg) {
@@ -764,6 +794,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     const bool have = tile < a.nseq;
     const bool fits = cur.C + 16 <= a.cap;
     TileState nxt = cur;
+    uint32_t sh = 0, aligned = 0;  // staging aligned to the output (offsets already published)
     if (VAR == BH_VARIANT_GAP && BH_INTERLEAVE_COUNT) {
       // count the next group's tile while decoding this group's tile
       const uint64_t ntile = gn * W + wib;
@@ -788,13 +819,21 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
         finish_count(nxt, par ^ 1);
       }
     } else {
-      // count the next group's tile, then decode this group's tile
+      // count the next group's tile, then decode this group's tile into
+      // staging aligned to its output (the group's offsets were published an
+      // iteration ago; wait only if they are not there yet)
       if (gn < ngroups) nxt = count_tile(gn * W + wib, bnext, wb_next, par ^ 1);
+      uint32_t ready = 0;
+      if (lane == 0) ready = *(volatile uint32_t*)&s_gen >= k + 1;
+      ready = __shfl_sync(0xffffffffu, ready, 0);
+      __threadfence_block();
+      if (ready) sh = (uint32_t)(*(volatile unsigned long long*)&s_Pw[par][wib]) & 7u;
       if (have && fits && cur.c) {
         SR r;
         r.init(base_s, cur.e);
-        if (!fdecode(r, cur.c, stg_s + 2 * cur.o, T)) bad = true;
+        if (!fdecode(r, cur.c, stg_s + 2 * ((ready ? sh : 0u) + cur.o), T)) bad = true;
       }
+      aligned = ready;
     }
     __syncwarp();
     // one warp (rotating, so no warp carries every look-back) publishes the
@@ -808,7 +847,8 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     __threadfence_block();
     const unsigned long long P = *(volatile unsigned long long*)&s_Pw[par][wib];
     if (have && fits) {
-      flush_compact(a.out, a.nsym, P, cur.C, stg_s);
+      if (aligned) flush_aligned_stg(a.out, a.nsym, P, cur.C, stg_s);
+      else flush_compact(a.out, a.nsym, P, cur.C, stg_s);
     } else if (have) {
       // reference rounds (staging.py:123-146) with capacity cap - 8
       const bool active = lane < cur.nsl;
