@@ -91,7 +91,8 @@ struct FusedArgs {
 constexpr uint32_t T_WL = 0;                      // uint2 [256][16] replicated wlut8
 constexpr uint32_t T_LIM = T_WL + 256 * 16 * 8;   // u64 [33]
 constexpr uint32_t T_BASE = T_LIM + 33 * 8;       // i64 [33]
-constexpr uint32_t T_END = T_BASE + 33 * 8;
+constexpr uint32_t T_L12 = T_BASE + 33 * 8;       // u32 [4096] second level: codes of 9..12 bits
+constexpr uint32_t T_END = T_L12 + 4 * FB_SIZE;
 
 __device__ __forceinline__ void tag_status(DevReport* rep, uint32_t ep, uint32_t status) {
   unsigned long long v = ((unsigned long long)ep << 32) | (unsigned long long)(0x7fffffffu - status);
@@ -175,6 +176,7 @@ struct SR {
 
 struct FTab {
   uint32_t wl;     // this lane's column of the replicated wlut8 (shared address)
+  uint32_t l12;    // shared address of lut12
   uint32_t lim;    // shared address of lim (u64[33])
   uint32_t base;   // shared address of base (i64[33])
   TableView t;
@@ -200,17 +202,23 @@ __device__ __noinline__ uint32_t fslow(uint32_t win, const uint32_t lim_s, const
   return slow_lookup(t, win);
 }
 
+// a code longer than 8 bits: shared 12-bit table, else the limit search
+__device__ __forceinline__ uint32_t flong(uint32_t win, const FTab& T) {
+  const uint32_t e = lds32(T.l12 + ((win >> (32 - FB)) << 2));
+  return e ? e : fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t);
+}
+
 // one codeword: sym | len<<16 (0 = no codeword matches)
 __device__ __forceinline__ uint32_t fone(uint32_t win, const FTab& T) {
   const uint2 w = lds64(T.wl + ((win >> 24) << 7));
   if (w.y) return (w.x & 0xffffu) | ((((w.y >> 21) & 7u) + 1) << 16);
-  return fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t);
+  return flong(win, T);
 }
 
 __device__ __forceinline__ uint32_t flen(uint32_t win, const FTab& T) {
   const uint32_t y = lds32(T.wl + ((win >> 24) << 7) + 4);
   if (y) return ((y >> 21) & 7u) + 1;
-  return (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t) >> 16) & 0xffu;
+  return (flong(win, T) >> 16) & 0xffu;
 }
 
 // count codewords starting in [pos, stop) (tile-relative); pos ends at the exit
@@ -263,7 +271,7 @@ __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const F
       k -= (int32_t)n;
       r.skip(((w.y >> 18) & 7u) + 1);
     } else {
-      const uint32_t e = fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t);
+      const uint32_t e = flong(win, T);
       const uint32_t len = (e >> 16) & 0xffu;
       if (!len) return false;
       sts16(dst, e);
@@ -671,6 +679,9 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     unsigned long long* s_lim = reinterpret_cast<unsigned long long*>(sm + T_LIM);
     long long* s_base = reinterpret_cast<long long*>(sm + T_BASE);
     for (int i = threadIdx.x; i < 33; i += blockDim.x) { s_lim[i] = gl[i]; s_base[i] = gb[i]; }
+    const uint4* g12 = reinterpret_cast<const uint4*>(tb_ + L.lut12);
+    uint4* s12 = reinterpret_cast<uint4*>(sm + T_L12);
+    for (int i = threadIdx.x; i < FB_SIZE / 4; i += blockDim.x) s12[i] = __ldg(g12 + i);
   }
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   FTab T;
@@ -678,6 +689,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
   T.wl = sm_s + T_WL + 8 * (lane & 15);
   T.lim = sm_s + T_LIM;
   T.base = sm_s + T_BASE;
+  T.l12 = sm_s + T_L12;
   T.t = table_view(a.table, a.max_codes, hdr->ncodes);
   T.kind = hdr->kind;
   __syncthreads();
