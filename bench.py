@@ -56,6 +56,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-extras", action="store_true", help="skip e2e/variants (profiling runs)")
     ap.add_argument("--fused", type=int, default=1)
+    ap.add_argument("--graph", type=int, default=1, help="replay the decode as a captured CUDA graph")
     return ap.parse_args()
 
 
@@ -412,18 +413,39 @@ def main():
     assert np.array_equal(dec.out[:n].cpu().numpy().view(np.uint16), codes), "decode mismatch"
 
     launches = count_launches(dec)
+    step_fn = dec
+    if args.graph:
+        # the fused decode is one kernel with its epoch kept on the device, so
+        # the whole call is capturable: replay removes host launch overhead
+        for _ in range(3):
+            dec()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            dec()
+        torch.cuda.synchronize()
+        step_fn = graph.replay
+        step_fn()
+        torch.cuda.synchronize()
+        assert np.array_equal(dec.out[:n].cpu().numpy().view(np.uint16), codes), "graph decode mismatch"
+        launches = count_launches(step_fn)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    _lib.profile_enable(True)
+    if not args.graph:
+        _lib.profile_enable(True)
     with ClockSampler(local) as clk:
         if world > 1:
             torch.distributed.barrier()
-        times = time_steps(dec, args.steps, args.warmup, flush)
+        times = time_steps(step_fn, args.steps, args.warmup, flush)
         if world > 1:
             torch.distributed.barrier()
-    prof = _lib.profile_read()
-    _lib.profile_enable(False)
+    if args.graph:
+        # one kernel per replay: the per-step events bracket exactly that launch
+        prof = {("fused_" + args.variant) if args.fused else "decode": (sum(times), len(times))}
+    else:
+        prof = _lib.profile_read()
+        _lib.profile_enable(False)
     r = dec.status()
     _lib.check(r.status, "bench decode")
     total_ms = sum(times)
@@ -462,6 +484,7 @@ def main():
             "l2": "256 MiB buffer rewritten between steps (outside the per-step events)",
             "parallelism": f"{world} field(s), one per GPU, no collective",
             "fused": bool(args.fused),
+            "cuda_graph": bool(args.graph),
         },
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": traffic, "alg_bytes_per_launch": ab,

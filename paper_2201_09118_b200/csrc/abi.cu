@@ -55,7 +55,9 @@ struct Ws {
   Ws(const bh_stream* s, const bh_tune* t) {
     uint64_t ns = nsub_of(s), nq = nseq_of(s);
     uint32_t C = (t && t->t_high) ? t->t_high + 1 : 1;
-    size_t o = 0;
+    // the fused path's epoch header and look-back descriptors come first and
+    // are never overwritten by this pipeline (their epochs must survive it)
+    size_t o = align16(bh_fused_workspace_bytes(s, 0, t));
     auto take = [&](size_t bytes) { size_t r = o; o = align16(o + bytes); return r; };
     entries = take(8 * ns);
     exits = take(8 * ns);
@@ -175,9 +177,8 @@ extern "C" const char* bh_status_string(int status) {
 
 extern "C" size_t bh_workspace_bytes(const bh_stream* s, int variant, const bh_tune* tune) {
   if (!s || !s->subseq_bits || !s->subseqs_per_seq) return 0;
-  size_t a = Ws(s, tune).total;
-  size_t b = bh_fused_workspace_bytes(s, variant, tune);
-  return a > b ? a : b;
+  (void)variant;
+  return Ws(s, tune).total;  // fused descriptors + the staged pipeline's arrays
 }
 
 // Reference-structured pipeline (every phase a separate kernel).

@@ -19,6 +19,7 @@ __global__ void k_report_init(DevReport* rep) {
     rep->bits_sync = rep->bits_count = rep->bits_write = 0;
     rep->write_rounds = rep->staged_slots = rep->bypass_slots = 0;
     rep->total_symbols = rep->stale_seams = rep->seam_passes = rep->repair_needed = 0;
+    rep->pad[0] = rep->pad[1] = rep->pad[2] = rep->pad[3] = 0;
   }
 }
 
@@ -577,11 +578,7 @@ extern "C" int bh_device_sm_count(void) { return sm_count(); }
 
 extern "C" size_t bh_report_bytes(void) { return sizeof(DevReport); }
 
-extern "C" void bh_fused_report_forget(const void* report_dev);
-extern "C" uint32_t bh_fused_report_epoch(const void* report_dev);
-
 extern "C" int bh_report_init(void* report_dev, void* cuda_stream) {
-  bh_fused_report_forget(report_dev);
   k_report_init<<<1, 32, 0, S(cuda_stream)>>>(static_cast<DevReport*>(report_dev));
   return last_status();
 }
@@ -592,8 +589,8 @@ extern "C" int bh_report_read(const void* report_dev, bh_report* out, void* cuda
     return BH_CUDA_ERROR;
   if (cudaStreamSynchronize(S(cuda_stream)) != cudaSuccess) return BH_CUDA_ERROR;
   out->status = r.status == 0x7fffffff ? BH_OK : r.status;
-  const uint32_t ep = bh_fused_report_epoch(report_dev);
-  if (ep) {  // written by a fused kernel: status is epoch-tagged in pad[0]
+  if (r.pad[2] == 0xF05EDull) {  // written by a fused kernel: status epoch-tagged in pad[0]
+    const uint32_t ep = (uint32_t)r.pad[1];
     const unsigned long long tag = r.pad[0];
     out->status = (uint32_t)(tag >> 32) == ep ? (int32_t)(0x7fffffffu - (uint32_t)tag) : BH_OK;
   }

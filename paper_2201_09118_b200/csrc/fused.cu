@@ -34,11 +34,10 @@
 //
 // No memory needs resetting between calls: descriptors and the report are
 // tagged with a per-call epoch (bh_workspace_reset once per allocation).
-#include <atomic>
-#include <chrono>
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include "common.cuh"
 
 namespace bh {
@@ -77,13 +76,15 @@ struct FusedArgs {
   unsigned long long* cnt_desc;
   unsigned long long* exit_desc;
   DevReport* rep;
-  uint32_t epoch;
+  unsigned int* ws_hdr;  // [0] epoch of the last completed call, [1] CTAs done
   uint32_t wpb;          // words per tile buffer (multiple of 4)
   uint32_t cap;          // staging symbols per warp (multiple of 8)
   uint32_t warps;        // warps per CTA
   uint32_t per_warp_bytes;
   uint32_t tables_bytes;
 };
+
+constexpr unsigned long long FUSED_MARK = 0xF05EDull;  // rep->pad[2]: report written by k_fused
 
 // shared-memory table layout inside the CTA (bytes)
 // wlut8 is replicated 16 times ([entry][16] uint2): an LDS.64 is served per
@@ -497,9 +498,9 @@ __device__ __forceinline__ void gap_window(const FusedArgs& a, uint64_t tile, ui
 // published final exit.
 template <int VAR>
 __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, uint64_t tile, uint32_t base_s,
-                                            uint64_t wb0, uint32_t nsl, uint32_t& e, uint32_t& c, bool& bad) {
+                                            uint64_t wb0, uint32_t nsl, uint32_t ep, uint32_t& e, uint32_t& c,
+                                            bool& bad) {
   const uint32_t lane = threadIdx.x & 31;
-  const uint32_t ep = a.epoch;
   const uint32_t sb = a.sb;
   const uint64_t j0 = tile * a.sps;
   const bool active = lane < nsl;
@@ -647,6 +648,24 @@ __device__ __forceinline__ bool count_decode2(SR& rc, uint32_t& pc, uint32_t sto
   return ok;
 }
 
+// Completion: the last CTA of the call records the epoch in the report and
+// advances the workspace epoch for the next call (stream-ordered, so the next
+// call -- or graph replay -- observes it).
+__device__ __forceinline__ void fused_finish(const FusedArgs& a, uint32_t ep) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned prev = atomicAdd(a.ws_hdr + 1, 1u);
+    if (prev == gridDim.x - 1) {
+      a.ws_hdr[1] = 0;
+      a.rep->pad[1] = ep;
+      a.rep->pad[2] = FUSED_MARK;
+      __threadfence();
+      *(volatile unsigned int*)a.ws_hdr = ep;
+    }
+  }
+}
+
 // One CTA processes a group of `warps` consecutive tiles per iteration (warp w
 // takes tile group*warps + w).  Software pipeline, per iteration k:
 //   count the tile of group k+1 (words staged one iteration ahead),
@@ -660,11 +679,16 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
   __shared__ uint32_t s_C[2][32];
   __shared__ unsigned long long s_Pw[2][32];
   __shared__ uint32_t s_arrive[2], s_gen;
+  // Per-call epoch kept on the device (graph-replayable): every CTA reads the
+  // epoch of the last completed call; the last CTA of this call to finish
+  // advances it (fused_finish), so all CTAs of one call agree.
+  const uint32_t ep = *(volatile const unsigned int*)a.ws_hdr + 1u;
   const TableHdr* hdr = static_cast<const TableHdr*>(a.table);
   if (VAR == BH_VARIANT_SYNC && !hdr->complete) {
     // the speculative windows differ from the reference's: only complete books
     // (where no window can fail) may take the fused path
-    if (blockIdx.x == 0 && threadIdx.x == 0) tag_status(a.rep, a.epoch, NEED_STAGED);
+    if (blockIdx.x == 0 && threadIdx.x == 0) tag_status(a.rep, ep, NEED_STAGED);
+    fused_finish(a, ep);
     return;
   }
   if (threadIdx.x == 0) { s_arrive[0] = 0; s_arrive[1] = 0; s_gen = 0; }
@@ -702,7 +726,6 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
   const uint32_t W = a.warps;
   const uint64_t ngroups = (a.nseq + W - 1) / W;
   const uint64_t G = gridDim.x;
-  const uint32_t ep = a.epoch;
   bool bad = false;
 
   // warp 0: wait for every warp's count of group `g` (arrivals are counted per
@@ -763,7 +786,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     s.nsl = 0;
     if (tile < a.nseq) {
       s.nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
-      tile_counts<VAR>(a, T, tile, wbase_s + 4 * a.wpb * buf, wb0, s.nsl, s.e, s.c, bad);
+      tile_counts<VAR>(a, T, tile, wbase_s + 4 * a.wpb * buf, wb0, s.nsl, ep, s.e, s.c, bad);
     }
     uint32_t incl = s.c;
     for (int off = 1; off < 32; off <<= 1) {
@@ -780,8 +803,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     return s;
   };
 
-  const uint64_t g0 = blockIdx.x;
-  if (g0 >= ngroups) return;
+  const uint64_t g0 = blockIdx.x;  // grid <= ngroups
   // prologue: stage groups g0 and g0+G, count g0, publish its offsets
   uint64_t wb_cur = 0, wb_next = 0, wb_nn = 0;
   if (g0 * W + wib < a.nseq) wb_cur = stage_words(a, g0 * W + wib, wbase);
@@ -909,6 +931,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
   }
   cp_wait<0>();
   if (__any_sync(0xffffffffu, bad) && lane == 0) tag_status(a.rep, ep, BH_INVALID);
+  fused_finish(a, ep);
 }
 
 }  // namespace bh
@@ -919,23 +942,8 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
 using namespace bh;
 
 namespace {
-std::atomic<uint32_t> g_epoch{0};
-std::mutex g_rep_mu;
-std::map<const void*, uint32_t> g_rep_epoch;  // report buffer -> epoch of its last fused launch
-
 inline uint64_t nsub_of(const bh_stream* s) { return (s->total_bits + s->subseq_bits - 1) / s->subseq_bits; }
 inline uint64_t nseq_of(const bh_stream* s) { return (nsub_of(s) + s->subseqs_per_seq - 1) / s->subseqs_per_seq; }
-
-uint32_t next_epoch() {
-  uint32_t e = g_epoch.fetch_add(1) + 1;
-  if (e == 1) {  // first use in this process: start somewhere unlikely to be stale
-    uint32_t seed = (uint32_t)std::chrono::steady_clock::now().time_since_epoch().count() | 1u;
-    g_epoch.store(seed + 1);
-    e = seed;
-  }
-  if ((e & EP_MASK) == 0) e = g_epoch.fetch_add(1) + 1;  // epoch 0 is "never written"
-  return e;
-}
 
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -971,6 +979,19 @@ FusedCfg fused_cfg(const bh_stream* s) {
     if (w < 1) w = 1;
   }
   if (w > 24) w = 24;
+  // small inputs: fewer warps per CTA so that every SM gets a group
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  const uint64_t nseq = nseq_of(s);
+  if (!env_int("BH_FUSED_WARPS", 0) && nseq < (uint64_t)sms * (uint64_t)w) {
+    w = (int)((nseq + sms - 1) / sms);
+    if (w < 2) w = 2;
+  }
   c.warps = (uint32_t)w;
   c.smem = c.tables + c.warps * c.per_warp;
   return c;
@@ -989,8 +1010,9 @@ extern "C" int bh_fused_supported(const bh_stream* s, int variant) {
   return c.smem <= 227 * 1024 ? 1 : 0;
 }
 
+// workspace: [64 B header: epoch, CTA-done counter][cnt desc][exit desc]
 extern "C" size_t bh_fused_workspace_bytes(const bh_stream* s, int, const bh_tune*) {
-  return 16 * nseq_of(s) + 256;
+  return 64 + 16 * nseq_of(s) + 256;
 }
 
 extern "C" int bh_workspace_reset(void* ws, size_t bytes, void* cuda_stream) {
@@ -1018,19 +1040,15 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.nsub = nsub_of(s);
   a.nseq = nseq;
   a.out = out_dev;
-  a.cnt_desc = static_cast<unsigned long long*>(ws);
+  a.ws_hdr = static_cast<unsigned int*>(ws);
+  a.cnt_desc = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 64);
   a.exit_desc = a.cnt_desc + nseq;
   a.rep = static_cast<DevReport*>(report_dev);
-  a.epoch = next_epoch();
   a.wpb = cfg.wpb;
   a.cap = cfg.cap;
   a.warps = cfg.warps;
   a.per_warp_bytes = cfg.per_warp;
   a.tables_bytes = cfg.tables;
-  {
-    std::lock_guard<std::mutex> g(g_rep_mu);
-    g_rep_epoch[report_dev] = a.epoch;
-  }
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -1038,12 +1056,32 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   const void* fn = variant == BH_VARIANT_GAP ? (const void*)k_fused<BH_VARIANT_GAP> : (const void*)k_fused<BH_VARIANT_SYNC>;
-  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem) != cudaSuccess)
-    return BH_CUDA_ERROR;
+  // launch attributes and occupancy cached per (kernel, threads, smem)
+  static std::mutex mu;
+  static std::map<std::tuple<const void*, uint32_t, uint32_t>, int> occ;
   int per_sm = 0;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)cfg.warps * 32, cfg.smem) != cudaSuccess ||
-      per_sm < 1)
-    return BH_CUDA_ERROR;
+  {
+    std::lock_guard<std::mutex> g(mu);
+    auto key = std::make_tuple(fn, cfg.warps, cfg.smem);
+    auto it = occ.find(key);
+    if (it == occ.end()) {
+      // the attribute is per kernel: raise it to the largest size ever cached
+      // (lowering it would break a cached larger configuration)
+      static std::map<const void*, uint32_t> smem_set;
+      uint32_t& cur = smem_set[fn];
+      if (cfg.smem > cur) {
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem) != cudaSuccess)
+          return BH_CUDA_ERROR;
+        cur = cfg.smem;
+      }
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, (int)cfg.warps * 32, cfg.smem) != cudaSuccess ||
+          per_sm < 1)
+        return BH_CUDA_ERROR;
+      occ[key] = per_sm;
+    } else {
+      per_sm = it->second;
+    }
+  }
   uint64_t grid = (uint64_t)per_sm * sms;
   const uint64_t need = (nseq + cfg.warps - 1) / cfg.warps;  // groups
   if (grid > need) grid = need;
@@ -1057,14 +1095,3 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   return cudaGetLastError() == cudaSuccess ? BH_OK : BH_CUDA_ERROR;
 }
 
-// epoch of the last fused launch that used this report buffer (0 = none)
-extern "C" uint32_t bh_fused_report_epoch(const void* report_dev) {
-  std::lock_guard<std::mutex> g(g_rep_mu);
-  auto it = g_rep_epoch.find(report_dev);
-  return it == g_rep_epoch.end() ? 0u : it->second;
-}
-
-extern "C" void bh_fused_report_forget(const void* report_dev) {
-  std::lock_guard<std::mutex> g(g_rep_mu);
-  g_rep_epoch.erase(report_dev);
-}
