@@ -33,12 +33,14 @@ import statistics
 import subprocess
 import sys
 import time
+import warnings
 from dataclasses import replace
 from pathlib import Path
 
 import numpy as np
 
 ROOT = Path(__file__).resolve().parent
+warnings.filterwarnings("ignore", message=".*Profiler clears events.*")
 sys.path.insert(0, str(ROOT))
 
 METRIC = "Huffman decode GB/s (decoded bytes)"

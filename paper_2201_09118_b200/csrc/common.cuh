@@ -36,11 +36,12 @@ struct TableHdr {
 
 // Fused-kernel tables:
 //   dlut8 u32[256]   next 8 bits -> sym | len<<16 for codes of <= 8 bits, else 0
-//   wlut8 uint2[256] next 8 bits -> up to 3 whole codewords for decoding plus
+//   wlut8 uint4[256] next 8 bits -> up to 6 whole codewords for decoding plus
 //                    the count of every whole codeword for counting:
-//                    x = s0 | s1<<16,  y = s2 | n<<16 | (bits-1)<<18 |
-//                    (len0-1)<<21 | ncount<<24 | (cbits-1)<<28
-//                    (y == 0: the first code is longer than 8 bits)
+//                    x = s0 | s1<<16, y = s2 | s3<<16, z = s4 | s5<<16,
+//                    w = bits | n<<4 | ncount<<8 | cbits<<12 | len0<<16
+//                    (n symbols in `bits` bits; ncount whole codewords in
+//                    cbits bits; w == 0: the first code is longer than 8 bits)
 //   clut8 u8[256]    next 8 bits -> (ncode<<3) | (bits-1) over every whole
 //                    codeword inside the 8 bits, 0 if the first one is longer
 //   lut12 u32[4096]  next 12 bits -> sym | len<<16 for codes of <= 12 bits, else 0
@@ -61,7 +62,7 @@ struct TableLayout {
     dlut8 = align16(cnt + sizeof(uint16_t) * LUT_SIZE);
     clut8 = dlut8 + 4 * 256;
     wlut8 = align16(clut8 + 256);
-    lut12 = align16(wlut8 + 8 * 256);
+    lut12 = align16(wlut8 + 16 * 256);
     lim = align16(lut12 + 4 * (size_t)FB_SIZE);
     base = lim + 8 * 33;
     lj = align16(base + 8 * 33);

@@ -43,11 +43,6 @@
 namespace bh {
 
 constexpr int HALO_WORDS = 8;
-// interleave the next tile's count with the current decode (gap variant):
-// measured slower on B200 (later count arrivals stall the pipelined look-back)
-#ifndef BH_INTERLEAVE_COUNT
-#define BH_INTERLEAVE_COUNT 0
-#endif
 constexpr int FUSED_MAX_THREADS = 768;  // <= 24 warps: up to 85 registers per thread
 constexpr uint32_t NEED_STAGED = 9;  // BH_NEED_STAGED
 
@@ -82,15 +77,16 @@ struct FusedArgs {
   uint32_t warps;        // warps per CTA
   uint32_t per_warp_bytes;
   uint32_t tables_bytes;
+  unsigned long long* trace;  // debug timeline (TR instantiation only)
 };
 
 constexpr unsigned long long FUSED_MARK = 0xF05EDull;  // rep->pad[2]: report written by k_fused
 
 // shared-memory table layout inside the CTA (bytes)
-// wlut8 is replicated 16 times ([entry][16] uint2): an LDS.64 is served per
-// half-warp, so lane l reading replica l%16 never conflicts (32 KB, not 64).
-constexpr uint32_t T_WL = 0;                      // uint2 [256][16] replicated wlut8
-constexpr uint32_t T_LIM = T_WL + 256 * 16 * 8;   // u64 [33]
+// wlut8 is replicated 8 times ([entry][8] uint4): an LDS.128 is served per
+// quarter-warp, so lane l reading replica l%8 never conflicts (32 KB).
+constexpr uint32_t T_WL = 0;                      // uint4 [256][8] replicated wlut8
+constexpr uint32_t T_LIM = T_WL + 256 * 8 * 16;   // u64 [33]
 constexpr uint32_t T_BASE = T_LIM + 33 * 8;       // i64 [33]
 constexpr uint32_t T_L12 = T_BASE + 33 * 8;       // u32 [4096] second level: codes of 9..12 bits
 constexpr uint32_t T_END = T_L12 + 4 * FB_SIZE;
@@ -211,26 +207,26 @@ __device__ __forceinline__ uint32_t flong(uint32_t win, const FTab& T) {
 
 // one codeword: sym | len<<16 (0 = no codeword matches)
 __device__ __forceinline__ uint32_t fone(uint32_t win, const FTab& T) {
-  const uint2 w = lds64(T.wl + ((win >> 24) << 7));
-  if (w.y) return (w.x & 0xffffu) | ((((w.y >> 21) & 7u) + 1) << 16);
+  const uint4 w = lds128(T.wl + ((win >> 24) << 7));
+  if (w.w) return (w.x & 0xffffu) | (((w.w >> 16) & 15u) << 16);
   return flong(win, T);
 }
 
 __device__ __forceinline__ uint32_t flen(uint32_t win, const FTab& T) {
-  const uint32_t y = lds32(T.wl + ((win >> 24) << 7) + 4);
-  if (y) return ((y >> 21) & 7u) + 1;
+  const uint32_t y = lds128(T.wl + ((win >> 24) << 7)).w;
+  if (y) return (y >> 16) & 15u;
   return (flong(win, T) >> 16) & 0xffu;
 }
 
 // count codewords starting in [pos, stop) (tile-relative); pos ends at the exit
 __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, const FTab& T, uint32_t& n) {
-  const uint32_t wy = pin(T.wl + 4);
+  const uint32_t wy = pin(T.wl);
   while (pos + 8 <= stop) {  // every whole codeword of the next 8 bits starts before stop
     const uint32_t win = r.peek();
-    const uint32_t y = lds32(wy + ((win >> 24) << 7));
+    const uint32_t y = lds128(wy + ((win >> 24) << 7)).w;
     if (!y) break;
-    const uint32_t b = (y >> 28) + 1;
-    n += (y >> 24) & 15u;
+    const uint32_t b = (y >> 12) & 15u;
+    n += (y >> 8) & 15u;
     r.skip(b);
     pos += b;
   }
@@ -243,10 +239,10 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
     if (pos + 8 <= stop) {  // back to the multi-codeword path after a long code
       while (pos + 8 <= stop) {
         const uint32_t win = r.peek();
-        const uint32_t y = lds32(wy + ((win >> 24) << 7));
+        const uint32_t y = lds128(wy + ((win >> 24) << 7)).w;
         if (!y) break;
-        const uint32_t b = (y >> 28) + 1;
-        n += (y >> 24) & 15u;
+        const uint32_t b = (y >> 12) & 15u;
+        n += (y >> 8) & 15u;
         r.skip(b);
         pos += b;
       }
@@ -262,15 +258,19 @@ __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const F
   int32_t k = (int32_t)c;
   while (k > 0) {
     const uint32_t win = r.peek();
-    const uint2 w = lds64(wl + ((win >> 24) << 7));
-    if (w.y) {
-      const uint32_t n = (w.y >> 16) & 3u;
+    const uint4 w = lds128(wl + ((win >> 24) << 7));
+    if (w.w) {
+      const int32_t n = (int32_t)((w.w >> 4) & 15u);
+      const int32_t m = n < k ? n : k;  // stores past the lane's range are predicated off
       sts16(dst, w.x);
-      if (n > 1 && k > 1) sts16(dst + 2, w.x >> 16);
-      if (n > 2 && k > 2) sts16(dst + 4, w.y);
-      dst += n << 1;
-      k -= (int32_t)n;
-      r.skip(((w.y >> 18) & 7u) + 1);
+      if (m > 1) sts16(dst + 2, w.x >> 16);
+      if (m > 2) sts16(dst + 4, w.y);
+      if (m > 3) sts16(dst + 6, w.y >> 16);
+      if (m > 4) sts16(dst + 8, w.z);
+      if (m > 5) sts16(dst + 10, w.z >> 16);
+      dst += (uint32_t)n << 1;
+      k -= n;
+      r.skip(w.w & 15u);
     } else {
       const uint32_t e = flong(win, T);
       const uint32_t len = (e >> 16) & 0xffu;
@@ -363,6 +363,44 @@ __device__ __forceinline__ unsigned long long lookback(unsigned long long* desc,
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16_ca(uint32_t s, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async8_ca(uint32_t s, const void* gmem) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(bar), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ uint32_t mbar_test(uint32_t bar, uint32_t parity) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}" : "=r"(r) : "r"(bar), "r"(parity) : "memory");
+  return r;
+}
+// bulk (TMA) copy global -> shared, completing on the mbarrier
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
+}
+__device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
@@ -598,56 +636,6 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
   if (!active) c = 0;
 }
 
-// GAP variant: the count chain of the next tile and the decode chain of the
-// current tile are independent, so one loop advances both (two dependent
-// chains per lane hide each other's shared-memory and ALU latency).
-// Count: codewords starting in [pc, stopc); decode: kd symbols to `dst`.
-__device__ __forceinline__ bool count_decode2(SR& rc, uint32_t& pc, uint32_t stopc, uint32_t& nc, SR& rd,
-                                              uint32_t kd_, uint32_t dst, const FTab& T) {
-  const uint32_t wl = pin(T.wl);
-  bool ok = true;
-  int32_t kd = (int32_t)kd_;
-  while (pc < stopc || kd > 0) {
-    if (pc < stopc) {
-      const uint32_t win = rc.peek();
-      const uint32_t y = lds32(wl + 4 + ((win >> 24) << 7));
-      uint32_t b;
-      if (y && pc + 8 <= stopc) {
-        nc += (y >> 24) & 15u;
-        b = (y >> 28) + 1;
-      } else {
-        b = y ? ((y >> 21) & 7u) + 1 : (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t) >> 16) & 0xffu;
-        nc += 1;
-        if (!b) { ok = false; b = stopc - pc; }  // unmatched pattern: stop this window
-      }
-      rc.skip(b < 32 ? b : 32);
-      pc += b;
-    }
-    if (kd > 0) {
-      const uint32_t win = rd.peek();
-      const uint2 w = lds64(wl + ((win >> 24) << 7));
-      if (w.y) {
-        const uint32_t n = (w.y >> 16) & 3u;
-        sts16(dst, w.x);
-        if (n > 1 && kd > 1) sts16(dst + 2, w.x >> 16);
-        if (n > 2 && kd > 2) sts16(dst + 4, w.y);
-        dst += n << 1;
-        kd -= (int32_t)n;
-        rd.skip(((w.y >> 18) & 7u) + 1);
-      } else {
-        const uint32_t e = fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t);
-        const uint32_t len = (e >> 16) & 0xffu;
-        if (!len) { ok = false; kd = 0; continue; }
-        sts16(dst, e);
-        dst += 2;
-        kd -= 1;
-        rd.skip(len);
-      }
-    }
-  }
-  return ok;
-}
-
 // Completion: the last CTA of the call records the epoch in the report and
 // advances the workspace epoch for the next call (stream-ordered, so the next
 // call -- or graph replay -- observes it).
@@ -673,12 +661,30 @@ __device__ __forceinline__ void fused_finish(const FusedArgs& a, uint32_t ep) {
 //   warp 0: look back for group k+1's output offset (a full iteration early),
 //   flush the tile of group k once group k's offset is published.
 // So the look-back latency never stalls the decode in steady state.
-template <int VAR>
+// debug timeline: per warp, TRACE_SLOTS globaltimer stamps (bh_debug_fused_trace)
+constexpr int TRACE_SLOTS = 64;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+template <int VAR, int TR>
 __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) {
+#define MARK(slot)                                                                                  \
+  do {                                                                                              \
+    if (TR && (threadIdx.x & 31) == 0 && (slot) < TRACE_SLOTS)                                      \
+      a.trace[((size_t)blockIdx.x * a.warps + (threadIdx.x >> 5)) * TRACE_SLOTS + (slot)] = gtime(); \
+  } while (0)
+  MARK(0);
   extern __shared__ __align__(16) unsigned char sm[];
   __shared__ uint32_t s_C[2][32];
   __shared__ unsigned long long s_Pw[2][32];
-  __shared__ uint32_t s_arrive[2], s_gen;
+  // mbarriers: [0] tables; [1+p] counts of this CTA's groups of parity p
+  // (W arrivals); [3+p] offsets of those groups published (1 arrival).  Group
+  // #m of the CTA uses parity p = m & 1 and phase (m >> 1) & 1: a warp can run
+  // at most one group ahead, so no barrier is ever two phases ahead of a waiter.
+  __shared__ __align__(8) unsigned long long s_mb[5];
   // Per-call epoch kept on the device (graph-replayable): every CTA reads the
   // epoch of the last completed call; the last CTA of this call to finish
   // advances it (fused_finish), so all CTAs of one call agree.
@@ -691,33 +697,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     fused_finish(a, ep);
     return;
   }
-  if (threadIdx.x == 0) { s_arrive[0] = 0; s_arrive[1] = 0; s_gen = 0; }
-  {
-    TableLayout L(a.max_codes);
-    const char* tb_ = static_cast<const char*>(a.table);
-    const uint2* wl = reinterpret_cast<const uint2*>(tb_ + L.wlut8);
-    uint2* s_wl = reinterpret_cast<uint2*>(sm + T_WL);
-    for (uint32_t i = threadIdx.x; i < 256 * 16; i += blockDim.x) s_wl[i] = __ldg(wl + (i >> 4));  // [ent][replica]
-    const unsigned long long* gl = reinterpret_cast<const unsigned long long*>(tb_ + L.lim);
-    const long long* gb = reinterpret_cast<const long long*>(tb_ + L.base);
-    unsigned long long* s_lim = reinterpret_cast<unsigned long long*>(sm + T_LIM);
-    long long* s_base = reinterpret_cast<long long*>(sm + T_BASE);
-    for (int i = threadIdx.x; i < 33; i += blockDim.x) { s_lim[i] = gl[i]; s_base[i] = gb[i]; }
-    const uint4* g12 = reinterpret_cast<const uint4*>(tb_ + L.lut12);
-    uint4* s12 = reinterpret_cast<uint4*>(sm + T_L12);
-    for (int i = threadIdx.x; i < FB_SIZE / 4; i += blockDim.x) s12[i] = __ldg(g12 + i);
-  }
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  FTab T;
-  const uint32_t sm_s = smem_u32(sm);
-  T.wl = sm_s + T_WL + 8 * (lane & 15);
-  T.lim = sm_s + T_LIM;
-  T.base = sm_s + T_BASE;
-  T.l12 = sm_s + T_L12;
-  T.t = table_view(a.table, a.max_codes, hdr->ncodes);
-  T.kind = hdr->kind;
-  __syncthreads();
-
   unsigned char* pw = sm + a.tables_bytes + (size_t)wib * a.per_warp_bytes;
   uint32_t* const wbase = reinterpret_cast<uint32_t*>(pw);
   const uint32_t wbase_s = smem_u32(pw);
@@ -726,17 +706,68 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
   const uint32_t W = a.warps;
   const uint64_t ngroups = (a.nseq + W - 1) / W;
   const uint64_t G = gridDim.x;
+  const uint64_t g0 = blockIdx.x;  // grid <= ngroups
   bool bad = false;
+
+  // The tables arrive by three bulk (TMA) copies -- one L2 request per line
+  // per CTA, where 148 CTAs x 8 replica loads of the same lines would queue on
+  // a few L2 slices -- while every warp's words for groups g0 and g0+G are in
+  // flight on cp.async.
+  const uint32_t sm_s = smem_u32(sm);
+  const uint32_t bar = smem_u32(&s_mb[0]);
+  const uint32_t bar_arr = bar + 8, bar_pub = bar + 24;  // + 8 * parity
+  if (threadIdx.x == 0) {
+    TableLayout L(a.max_codes);
+    const char* tb_ = static_cast<const char*>(a.table);
+    mbar_init(bar, 1);
+    mbar_init(bar_arr, W);
+    mbar_init(bar_arr + 8, W);
+    mbar_init(bar_pub, 1);
+    mbar_init(bar_pub + 8, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(bar, 4096 + 528 + 4 * FB_SIZE);
+    bulk_g2s(sm_s + T_WL, tb_ + L.wlut8, 4096, bar);  // entries packed, spread below
+    bulk_g2s(sm_s + T_LIM, tb_ + L.lim, 528, bar);    // lim, base (contiguous)
+    bulk_g2s(sm_s + T_L12, tb_ + L.lut12, 4 * FB_SIZE, bar);
+  }
+  uint64_t wb_cur = 0, wb_next = 0, wb_nn = 0;
+  if (g0 * W + wib < a.nseq) wb_cur = stage_words(a, g0 * W + wib, wbase);
+  cp_commit();
+  if ((g0 + G) * W + wib < a.nseq) wb_next = stage_words(a, (g0 + G) * W + wib, wbase + a.wpb);
+  cp_commit();
+  __syncthreads();  // barrier initialised
+  MARK(TRACE_SLOTS - 5);
+  mbar_wait(bar, 0);
+  MARK(TRACE_SLOTS - 4);
+  // spread wlut8 into its 8 replicas ([entry][replica] uint4), highest entries
+  // first: entry e's replicas overwrite packed entries >= e only
+  for (int hi = 255; hi >= 0; hi -= (int)blockDim.x) {
+    const int e = hi - (int)threadIdx.x;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (e >= 0) v = lds128(sm_s + T_WL + 16 * e);
+    __syncthreads();
+    if (e >= 0)
+      for (uint32_t r = 0; r < 8; ++r) sts128(sm_s + T_WL + 128 * e + 16 * r, v);
+    __syncthreads();
+  }
+  FTab T;
+  T.wl = sm_s + T_WL + 16 * (lane & 7);
+  T.lim = sm_s + T_LIM;
+  T.base = sm_s + T_BASE;
+  T.l12 = sm_s + T_L12;
+  T.t = table_view(a.table, a.max_codes, hdr->ncodes);
+  T.kind = hdr->kind;
+  MARK(TRACE_SLOTS - 3);
+  cp_wait<1>();  // group g0's words
+  __syncthreads();
+  MARK(1);
 
   // warp 0: wait for every warp's count of group `g` (arrivals are counted per
   // group parity: a fast warp can run at most one group ahead), look back,
   // publish per-warp output offsets into s_Pw[par].
-  auto publish = [&](uint64_t g, uint32_t par, uint32_t arrivals, uint32_t gen) {
-    if (lane == 0) {
-      while (*(volatile uint32_t*)&s_arrive[par] < arrivals) __nanosleep(20);
-    }
-    __syncwarp();
-    __threadfence_block();
+  auto publish = [&](uint64_t g, uint32_t m) {  // group #m of this CTA
+    const uint32_t par = m & 1;
+    mbar_wait(bar_arr + 8 * par, (m >> 1) & 1);
     const uint32_t v = lane < W ? *(volatile uint32_t*)&s_C[par][lane] : 0u;
     uint32_t pre = v;
     for (int off = 1; off < 32; off <<= 1) {
@@ -759,25 +790,11 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     }
     __threadfence_block();
     __syncwarp();
-    if (lane == 0) *(volatile uint32_t*)&s_gen = gen;
+    if (lane == 0) mbar_arrive(bar_pub + 8 * par);
   };
 
   // per-tile state kept across the pipeline
   struct TileState { uint32_t e, c, o, C, nsl; uint64_t wb0; };
-  auto finish_count = [&](TileState& s, uint32_t par) {
-    uint32_t incl = s.c;
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-      if ((int)lane >= off) incl += y;
-    }
-    s.C = __shfl_sync(0xffffffffu, incl, 31);
-    s.o = incl - s.c;
-    if (lane == 0) {
-      s_C[par][wib] = s.C;
-      __threadfence_block();
-      atomicAdd(&s_arrive[par], 1u);
-    }
-  };
   auto count_tile = [&](uint64_t tile, uint32_t buf, uint64_t wb0, uint32_t par) -> TileState {
     TileState s;
     s.wb0 = wb0;
@@ -797,23 +814,16 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     s.o = incl - s.c;
     if (lane == 0) {
       s_C[par][wib] = s.C;
-      __threadfence_block();
-      atomicAdd(&s_arrive[par], 1u);
+      mbar_arrive(bar_arr + 8 * par);  // release: s_C visible to the publisher
     }
     return s;
   };
 
-  const uint64_t g0 = blockIdx.x;  // grid <= ngroups
-  // prologue: stage groups g0 and g0+G, count g0, publish its offsets
-  uint64_t wb_cur = 0, wb_next = 0, wb_nn = 0;
-  if (g0 * W + wib < a.nseq) wb_cur = stage_words(a, g0 * W + wib, wbase);
-  cp_commit();
-  if ((g0 + G) * W + wib < a.nseq) wb_next = stage_words(a, (g0 + G) * W + wib, wbase + a.wpb);
-  cp_commit();
-  cp_wait<1>();
-  __syncwarp();
+  // prologue: count g0, publish its offsets
   TileState cur = count_tile(g0 * W + wib, 0, wb_cur, 0);
-  if (wib == 0) publish(g0, 0, W, 1);  // group #0 of this CTA: parity 0, 1st occurrence
+  MARK(2);
+  if (wib == 0) publish(g0, 0);
+  MARK(3);
 
   uint32_t k = 0, bcur = 0, bnext = 1, bnn = 2;
   for (uint64_t g = g0; g < ngroups; g += G, ++k) {
@@ -829,56 +839,28 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     const bool fits = cur.C + 16 <= a.cap;
     TileState nxt = cur;
     uint32_t sh = 0, aligned = 0;  // staging aligned to the output (offsets already published)
-    if (VAR == BH_VARIANT_GAP && BH_INTERLEAVE_COUNT) {
-      // count the next group's tile while decoding this group's tile
-      const uint64_t ntile = gn * W + wib;
-      const bool nhave = gn < ngroups && ntile < a.nseq;
-      uint32_t nsl = 0, ne = 0, nstop = 0;
-      if (nhave) {
-        nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - ntile * a.sps);
-        gap_window(a, ntile, wb_next, nsl, ne, nstop);
-      }
-      SR rc, rd;
-      uint32_t pc = ne, nc = 0;
-      if (nhave && lane < nsl && ne < nstop) rc.init(wbase_s + 4 * a.wpb * bnext, ne);
-      else nstop = pc;  // nothing to count
-      const uint32_t kd = (have && fits && cur.c) ? cur.c : 0u;
-      if (kd) rd.init(base_s, cur.e);
-      if (!count_decode2(rc, pc, nstop, nc, rd, kd, stg_s + 2 * cur.o, T)) bad = true;
-      if (gn < ngroups) {
-        nxt.wb0 = wb_next;
-        nxt.e = ne;
-        nxt.c = (nhave && lane < nsl) ? nc : 0u;
-        nxt.nsl = nsl;
-        finish_count(nxt, par ^ 1);
-      }
-    } else {
-      // count the next group's tile, then decode this group's tile into
-      // staging aligned to its output (the group's offsets were published an
-      // iteration ago; wait only if they are not there yet)
-      if (gn < ngroups) nxt = count_tile(gn * W + wib, bnext, wb_next, par ^ 1);
-      uint32_t ready = 0;
-      if (lane == 0) ready = *(volatile uint32_t*)&s_gen >= k + 1;
-      ready = __shfl_sync(0xffffffffu, ready, 0);
-      __threadfence_block();
-      if (ready) sh = (uint32_t)(*(volatile unsigned long long*)&s_Pw[par][wib]) & 7u;
-      if (have && fits && cur.c) {
-        SR r;
-        r.init(base_s, cur.e);
-        if (!fdecode(r, cur.c, stg_s + 2 * ((ready ? sh : 0u) + cur.o), T)) bad = true;
-      }
-      aligned = ready;
+    // count the next group's tile, then decode this group's tile into
+    // staging aligned to its output (the group's offsets were published an
+    // iteration ago; wait only if they are not there yet)
+    if (gn < ngroups) nxt = count_tile(gn * W + wib, bnext, wb_next, par ^ 1);
+    MARK(4 + 5 * k);
+    const uint32_t ready = __shfl_sync(0xffffffffu, lane == 0 ? mbar_test(bar_pub + 8 * par, (k >> 1) & 1) : 0u, 0);
+    if (ready) sh = (uint32_t)(*(volatile unsigned long long*)&s_Pw[par][wib]) & 7u;
+    if (have && fits && cur.c) {
+      SR r;
+      r.init(base_s, cur.e);
+      if (!fdecode(r, cur.c, stg_s + 2 * ((ready ? sh : 0u) + cur.o), T)) bad = true;
     }
+    aligned = ready;
     __syncwarp();
+    MARK(5 + 5 * k);
     // one warp (rotating, so no warp carries every look-back) publishes the
     // next group's offsets -- needed one iteration from now
-    if (wib == (k + 1) % W && gn < ngroups) publish(gn, par ^ 1, ((k + 1) / 2 + 1) * W, k + 2);  // group #k+1
+    if (wib == (k + 1) % W && gn < ngroups) publish(gn, k + 1);
+    MARK(6 + 5 * k);
     // flush once this group's offsets are published
-    if (lane == 0) {
-      while (*(volatile uint32_t*)&s_gen < k + 1) __nanosleep(20);
-    }
-    __syncwarp();
-    __threadfence_block();
+    mbar_wait(bar_pub + 8 * par, (k >> 1) & 1);
+    MARK(7 + 5 * k);
     const unsigned long long P = *(volatile unsigned long long*)&s_Pw[par][wib];
     if (have && fits) {
       if (aligned) flush_aligned_stg(a.out, a.nsym, P, cur.C, stg_s);
@@ -921,6 +903,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
       }
     }
     __syncwarp();
+    MARK(8 + 5 * k);
     cur = nxt;
     wb_cur = wb_next;
     wb_next = wb_nn;
@@ -931,7 +914,10 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
   }
   cp_wait<0>();
   if (__any_sync(0xffffffffu, bad) && lane == 0) tag_status(a.rep, ep, BH_INVALID);
+  MARK(TRACE_SLOTS - 2);
   fused_finish(a, ep);
+  MARK(TRACE_SLOTS - 1);
+#undef MARK
 }
 
 }  // namespace bh
@@ -999,6 +985,22 @@ FusedCfg fused_cfg(const bh_stream* s) {
 
 }  // namespace
 
+static unsigned long long* g_trace = nullptr;
+
+// Debug: record a per-warp timeline of the next fused launches into trace_dev
+// (u64[grid * warps * 64] globaltimer stamps); NULL switches it off.
+extern "C" int bh_debug_fused_trace(void* trace_dev) {
+  g_trace = static_cast<unsigned long long*>(trace_dev);
+  return BH_OK;
+}
+
+extern "C" int bh_debug_fused_shape(const bh_stream* s, uint32_t* warps, uint32_t* smem) {
+  FusedCfg c = fused_cfg(s);
+  if (warps) *warps = c.warps;
+  if (smem) *smem = c.smem;
+  return BH_OK;
+}
+
 extern "C" int bh_fused_supported(const bh_stream* s, int variant) {
   if (env_int("BH_DISABLE_FUSED", 0)) return 0;
   if (variant != BH_VARIANT_GAP && variant != BH_VARIANT_SYNC) return 0;
@@ -1055,7 +1057,9 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
-  const void* fn = variant == BH_VARIANT_GAP ? (const void*)k_fused<BH_VARIANT_GAP> : (const void*)k_fused<BH_VARIANT_SYNC>;
+  a.trace = g_trace;
+  const void* fn = variant == BH_VARIANT_GAP ? (g_trace ? (const void*)k_fused<BH_VARIANT_GAP, 1> : (const void*)k_fused<BH_VARIANT_GAP, 0>)
+                                             : (g_trace ? (const void*)k_fused<BH_VARIANT_SYNC, 1> : (const void*)k_fused<BH_VARIANT_SYNC, 0>);
   // launch attributes and occupancy cached per (kernel, threads, smem)
   static std::mutex mu;
   static std::map<std::tuple<const void*, uint32_t, uint32_t>, int> occ;
@@ -1087,10 +1091,10 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   if (grid > need) grid = need;
   if (grid < 1) grid = 1;
   prof_mark(static_cast<cudaStream_t>(cuda_stream), "start");
-  if (variant == BH_VARIANT_GAP)
-    k_fused<BH_VARIANT_GAP><<<(unsigned)grid, cfg.warps * 32, cfg.smem, static_cast<cudaStream_t>(cuda_stream)>>>(a);
-  else
-    k_fused<BH_VARIANT_SYNC><<<(unsigned)grid, cfg.warps * 32, cfg.smem, static_cast<cudaStream_t>(cuda_stream)>>>(a);
+  void* args[] = {&a};
+  if (cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(cfg.warps * 32), args, cfg.smem,
+                       static_cast<cudaStream_t>(cuda_stream)) != cudaSuccess)
+    return BH_CUDA_ERROR;
   prof_mark(static_cast<cudaStream_t>(cuda_stream), variant == BH_VARIANT_GAP ? "fused_gap" : "fused_sync");
   return cudaGetLastError() == cudaSuccess ? BH_OK : BH_CUDA_ERROR;
 }

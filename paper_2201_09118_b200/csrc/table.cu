@@ -222,22 +222,22 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
       ++n;
     }
     clut8[v] = n ? (uint8_t)((n << 3) | (pos - 1)) : (uint8_t)0;
-    // up to three whole codewords of the 8-bit window, for the decode-write pass
-    uint32_t p3 = 0, n3 = 0, sy[3] = {0, 0, 0}, l0 = 0;
-    while (n3 < 3 && p3 < 8) {
-      uint32_t f = slow_lookup(t, ((uint32_t)v << 24) << p3);
+    // up to six whole codewords of the 8-bit window, for the decode-write pass
+    uint32_t p6 = 0, n6 = 0, sy[6] = {0, 0, 0, 0, 0, 0}, l0 = 0;
+    while (n6 < 6 && p6 < 8) {
+      uint32_t f = slow_lookup(t, ((uint32_t)v << 24) << p6);
       uint32_t len = (f >> 16) & 0xff;
-      if (len == 0 || p3 + len > 8) break;
-      if (n3 == 0) l0 = len;
-      sy[n3++] = f & 0xffff;
-      p3 += len;
+      if (len == 0 || p6 + len > 8) break;
+      if (n6 == 0) l0 = len;
+      sy[n6++] = f & 0xffff;
+      p6 += len;
     }
-    uint2 wl;
+    uint4 wl;
     wl.x = sy[0] | (sy[1] << 16);
-    // y = s2 | n<<16 | (bits-1)<<18 | (len0-1)<<21 | ncount<<24 | (cbits-1)<<28
-    wl.y = n3 ? (sy[2] | (n3 << 16) | ((p3 - 1) << 18) | ((l0 - 1) << 21) | (n << 24) | ((pos - 1) << 28))
-              : 0u;
-    reinterpret_cast<uint2*>(reinterpret_cast<char*>(blob) + L.wlut8)[v] = wl;
+    wl.y = sy[2] | (sy[3] << 16);
+    wl.z = sy[4] | (sy[5] << 16);
+    wl.w = n6 ? (p6 | (n6 << 4) | (n << 8) | (pos << 12) | (l0 << 16)) : 0u;
+    reinterpret_cast<uint4*>(reinterpret_cast<char*>(blob) + L.wlut8)[v] = wl;
   }
 }
 
