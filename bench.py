@@ -168,13 +168,13 @@ class Decoder:
         self.lib = _lib.load()
         self.ds = device_stream(stream)
         self.variant = _lib.VARIANT_GAP if variant == "gap" else _lib.VARIANT_SYNC
-        self.tune = make_tune(3584, tuner, False, fused)
+        self.tune = make_tune(3584, tuner, False, fused, max_len=stream.codebook.max_len)
         self.out = empty(stream.symbol_count, np.uint16, self.ds.device)
         self.wsb = self.lib.bh_workspace_bytes(self.ds.ref, self.variant, C.byref(self.tune))
         self.ws = torch.empty(max(self.wsb, 256), dtype=torch.uint8, device=self.ds.device)
         from paper_2201_09118_b200._lib import stream_handle
         self.lib.bh_workspace_reset(self.ws.data_ptr(), self.ws.numel(), stream_handle())
-        self.rep = DeviceReport(self.ds.device)
+        self.rep = DeviceReport(self.ds.device).init()
 
     def __call__(self):
         from paper_2201_09118_b200._lib import check, stream_handle
@@ -245,11 +245,11 @@ def e2e_measure(stream, book, variant: str, steps: int, flush):
     cs = _lib.Stream(words.data_ptr(), stream.total_bits, stream.symbol_count, lay.subseq_bits,
                      lay.subseqs_per_seq, 16, max_codes, gap_d.data_ptr(), table.data_ptr())
     var = _lib.VARIANT_GAP if variant == "gap" else _lib.VARIANT_SYNC
-    tune = make_tune()
+    tune = make_tune(max_len=stream.codebook.max_len)
     wsb = lib.bh_workspace_bytes(C.byref(cs), var, C.byref(tune))
     ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)
     lib.bh_workspace_reset(ws.data_ptr(), ws.numel(), stream_handle())
-    rep = DeviceReport(dev)
+    rep = DeviceReport(dev).init()
 
     def step():
         st = stream_handle()

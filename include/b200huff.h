@@ -62,6 +62,9 @@ typedef struct bh_tune {
     uint32_t collect_stats;      /* fill bits/rounds/staged/bypass (slower) */
     uint32_t fused;              /* 1 = single-pass fused kernels (default), 0 = staged pipeline */
     uint32_t seam_passes;        /* pre-launched seam passes before the status read (>=1) */
+    uint32_t max_len;            /* longest code length when known (0 = unknown); <= 8 lets the
+                                    fused kernel leave the 12-bit second-level table out of
+                                    shared memory (more warps per SM) */
 } bh_tune;
 
 /* Decode report, mirroring DecodeStats (staging.py:31-45) plus status. */
@@ -103,7 +106,10 @@ int bh_canonical_codes(const uint8_t *lengths_dev, uint32_t alphabet, uint32_t *
 /* ---- whole-decoder entry point (sync_decoder.decode / gap_decoder.decode) */
 size_t bh_workspace_bytes(const bh_stream *s, int variant, const bh_tune *tune);
 /* Decodes symbol_count symbols into out_dev (uint16).  report_dev receives a
- * device-side report; nothing is synchronised.  bh_report_read copies it. */
+ * device-side report; nothing is synchronised.  bh_report_read copies it.
+ * A report buffer must be initialised (bh_report_init) once before its first
+ * use: the fused kernels tag their status with a per-call epoch and never
+ * reset it, so repeated (or graph-replayed) calls need no further init. */
 int bh_decode_async(const bh_stream *s, int variant, const bh_tune *tune, uint16_t *out_dev,
                     void *workspace_dev, size_t workspace_bytes, void *report_dev,
                     void *cuda_stream);

@@ -39,6 +39,7 @@ class Tune(C.Structure):
     _fields_ = [
         ("t_high", U32), ("capacity", U32), ("capacity_table", U32 * 64),
         ("early_exit", U32), ("collect_stats", U32), ("fused", U32), ("seam_passes", U32),
+        ("max_len", U32),
     ]
 
 
@@ -107,7 +108,8 @@ def load():
                 f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
                 "or `make -C paper_2201_09118_b200/csrc` (there is no CPU fallback)"
             )
-        lib = C.CDLL(str(LIB_PATH))
+        # BH_LIB: load an alternative build of the same library (A/B experiments)
+        lib = C.CDLL(os.environ.get("BH_LIB") or str(LIB_PATH))
         for name, (res, args) in SIGNATURES.items():
             fn = getattr(lib, name)
             fn.restype = res

@@ -303,7 +303,12 @@ extern "C" int bh_decode(const bh_stream* s, int variant, const bh_tune* tune, u
   size_t need = bh_workspace_bytes(s, variant, tune);
   if (ws_bytes < need + align16(bh_report_bytes())) return BH_BAD_ARGUMENT;
   void* rep = static_cast<char*>(ws) + align16(need);
-  int rc = bh_decode_async(s, variant, tune, out_dev, ws, need, rep, cuda_stream);
+  // the slot may hold another call's scratch (its position follows this
+  // stream's workspace size): the fused kernels' epoch-tagged status must
+  // start from a clean report
+  int rc = bh_report_init(rep, cuda_stream);
+  if (rc) return rc;
+  rc = bh_decode_async(s, variant, tune, out_dev, ws, need, rep, cuda_stream);
   if (rc) return rc;
   bh_report r;
   memset(&r, 0, sizeof(r));

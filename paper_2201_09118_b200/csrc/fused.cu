@@ -70,6 +70,9 @@ struct FusedArgs {
   uint16_t* out;
   unsigned long long* cnt_desc;
   unsigned long long* exit_desc;
+  uint32_t* lane_info;   // two-phase kernel: per subsequence (entry - boundary) | lane prefix << 16
+  uint32_t* tile_cnt;    // two-phase kernel: symbols per tile
+  uint32_t* tile_off;    // two-phase kernel: exclusive tile offset within its CTA's range
   DevReport* rep;
   unsigned int* ws_hdr;  // [0] epoch of the last completed call, [1] CTAs done
   uint32_t wpb;          // words per tile buffer (multiple of 4)
@@ -77,6 +80,7 @@ struct FusedArgs {
   uint32_t warps;        // warps per CTA
   uint32_t per_warp_bytes;
   uint32_t tables_bytes;
+  uint32_t has_l12;      // 12-bit second-level table staged (codes longer than 8 bits)
   unsigned long long* trace;  // debug timeline (TR instantiation only)
 };
 
@@ -88,7 +92,9 @@ constexpr unsigned long long FUSED_MARK = 0xF05EDull;  // rep->pad[2]: report wr
 constexpr uint32_t T_WL = 0;                      // uint4 [256][8] replicated wlut8
 constexpr uint32_t T_LIM = T_WL + 256 * 8 * 16;   // u64 [33]
 constexpr uint32_t T_BASE = T_LIM + 33 * 8;       // i64 [33]
-constexpr uint32_t T_L12 = T_BASE + 33 * 8;       // u32 [4096] second level: codes of 9..12 bits
+constexpr uint32_t T_C12 = T_BASE + 33 * 8;       // u16 [4096] 12-bit count table
+constexpr uint32_t T_L12 = T_C12 + 2 * FB_SIZE;   // u32 [4096] second level: codes of 9..12 bits (optional)
+constexpr uint32_t T_END_NOL12 = T_L12;
 constexpr uint32_t T_END = T_L12 + 4 * FB_SIZE;
 
 __device__ __forceinline__ void tag_status(DevReport* rep, uint32_t ep, uint32_t status) {
@@ -174,6 +180,7 @@ struct SR {
 struct FTab {
   uint32_t wl;     // this lane's column of the replicated wlut8 (shared address)
   uint32_t l12;    // shared address of lut12
+  uint32_t c12;    // shared address of clut12
   uint32_t lim;    // shared address of lim (u64[33])
   uint32_t base;   // shared address of base (i64[33])
   TableView t;
@@ -201,7 +208,7 @@ __device__ __noinline__ uint32_t fslow(uint32_t win, const uint32_t lim_s, const
 
 // a code longer than 8 bits: shared 12-bit table, else the limit search
 __device__ __forceinline__ uint32_t flong(uint32_t win, const FTab& T) {
-  const uint32_t e = lds32(T.l12 + ((win >> (32 - FB)) << 2));
+  const uint32_t e = T.l12 ? lds32(T.l12 + ((win >> (32 - FB)) << 2)) : 0u;
   return e ? e : fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t);
 }
 
@@ -218,50 +225,93 @@ __device__ __forceinline__ uint32_t flen(uint32_t win, const FTab& T) {
   return (flong(win, T) >> 16) & 0xffu;
 }
 
-// count codewords starting in [pos, stop) (tile-relative); pos ends at the exit
-__device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, const FTab& T, uint32_t& n) {
-  const uint32_t wy = pin(T.wl);
-  while (pos + 8 <= stop) {  // every whole codeword of the next 8 bits starts before stop
-    const uint32_t win = r.peek();
-    const uint32_t y = lds128(wy + ((win >> 24) << 7)).w;
-    if (!y) break;
-    const uint32_t b = (y >> 12) & 15u;
-    n += (y >> 8) & 15u;
-    r.skip(b);
-    pos += b;
+// length of one codeword from the 12-bit count table (second start, or the end
+// of the only whole codeword); codes longer than 12 bits take the limit search
+__device__ __forceinline__ uint32_t clen(uint32_t win, const FTab& T) {
+  const uint32_t y = lds16(T.c12 + ((win >> (32 - FB)) << 1));
+  if (y) {
+    const uint32_t m = y & 0xffeu;
+    return m ? __ffs(m) - 1 : (y >> 12);
   }
+  return (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t) >> 16) & 0xffu;
+}
+
+// count codewords starting in [pos, stop) (tile-relative); pos ends at the exit.
+// 12-bit count table: every whole codeword of the next 12 bits per lookup
+// (popcount of the start mask).  The one lookup that crosses `stop` counts the
+// starts below it and exits at the first start at or past it; a code longer
+// than 12 bits takes one codeword.
+__device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, const FTab& T, uint32_t& n) {
+  const uint32_t ct = pin(T.c12);
   while (pos < stop) {
-    const uint32_t len = flen(r.peek(), T);
-    if (!len) return false;
-    r.skip(len);
-    pos += len;
-    ++n;
-    if (pos + 8 <= stop) {  // back to the multi-codeword path after a long code
-      while (pos + 8 <= stop) {
-        const uint32_t win = r.peek();
-        const uint32_t y = lds128(wy + ((win >> 24) << 7)).w;
-        if (!y) break;
-        const uint32_t b = (y >> 12) & 15u;
-        n += (y >> 8) & 15u;
-        r.skip(b);
-        pos += b;
+    const uint32_t win = r.peek();
+    const uint32_t y = lds16(ct + ((win >> (32 - FB)) << 1));
+    const uint32_t b = y >> 12;
+    if (pos + b <= stop) {
+      if (!y) {  // first code longer than 12 bits
+        const uint32_t l = (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t) >> 16) & 0xffu;
+        if (!l) return false;
+        n += 1;
+        r.skip(l);
+        pos += l;
+        continue;
       }
+      n += __popc(y & 0xfffu);
+      r.skip(b);
+      pos += b;
+    } else {  // the window ends inside this entry (stop - pos < b <= 12)
+      const uint32_t rem = stop - pos;
+      const uint32_t mask = y & 0xfffu;
+      n += __popc(mask & ((1u << rem) - 1u));
+      const uint32_t hi = mask >> rem;
+      const uint32_t adv = hi ? rem + __ffs(hi) - 1 : b;
+      r.skip(adv);
+      pos += adv;
     }
   }
   return true;
 }
 
-// Decode c (>= 1) symbols into compact staging at `dst` (lane ranges are
-// disjoint; stores past the lane's own range are predicated off).
+// Decode c (>= 1) symbols into compact staging at `dst`.  While at least six
+// symbols remain, all six symbols of a table entry are stored unconditionally
+// (the ones past the entry's count land inside the lane's own range and are
+// overwritten by its next stores); the last entries store predicated, so lane
+// ranges stay disjoint even for corrupt (non-contiguous) windows.
 __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const FTab& T) {
   const uint32_t wl = pin(T.wl);
   int32_t k = (int32_t)c;
+#ifndef BH_FDEC_PRED
+  while (k >= 6) {
+    const uint32_t win = r.peek();
+    const uint4 w = lds128(wl + ((win >> 24) << 7));
+    if (w.w) {
+      sts16(dst, w.x);
+      sts16(dst + 2, w.x >> 16);
+      sts16(dst + 4, w.y);
+      sts16(dst + 6, w.y >> 16);
+      sts16(dst + 8, w.z);
+      sts16(dst + 10, w.z >> 16);
+      const int32_t n = (int32_t)((w.w >> 4) & 15u);
+      dst += (uint32_t)n << 1;
+      k -= n;
+      r.skip(w.w & 15u);
+    } else {
+      const uint32_t e = flong(win, T);
+      const uint32_t len = (e >> 16) & 0xffu;
+      if (!len) return false;
+      sts16(dst, e);
+      dst += 2;
+      k -= 1;
+      r.skip(len);
+    }
+  }
+#endif
   while (k > 0) {
     const uint32_t win = r.peek();
     const uint4 w = lds128(wl + ((win >> 24) << 7));
     if (w.w) {
       const int32_t n = (int32_t)((w.w >> 4) & 15u);
-      const int32_t m = n < k ? n : k;  // stores past the lane's range are predicated off
+      const int32_t m = n < k ? n : k;
       sts16(dst, w.x);
       if (m > 1) sts16(dst + 2, w.x >> 16);
       if (m > 2) sts16(dst + 4, w.y);
@@ -320,13 +370,13 @@ __device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co
     if (pn >= stop) { cn = nn; xn = pn; return true; }
     if (po == pn) { cn = nn + (co - no); xn = xo; return true; }
     if (po < pn) {
-      const uint32_t l = flen(ro.peek(), T);
+      const uint32_t l = clen(ro.peek(), T);
       if (!l) return false;
       ro.skip(l);
       po += l;
       ++no;
     } else {
-      const uint32_t l = flen(rn.peek(), T);
+      const uint32_t l = clen(rn.peek(), T);
       if (!l) return false;
       rn.skip(l);
       pn += l;
@@ -725,10 +775,11 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
     mbar_init(bar_pub, 1);
     mbar_init(bar_pub + 8, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(bar, 4096 + 528 + 4 * FB_SIZE);
+    mbar_expect_tx(bar, 4096 + 528 + 2 * FB_SIZE + (a.has_l12 ? 4 * FB_SIZE : 0));
     bulk_g2s(sm_s + T_WL, tb_ + L.wlut8, 4096, bar);  // entries packed, spread below
     bulk_g2s(sm_s + T_LIM, tb_ + L.lim, 528, bar);    // lim, base (contiguous)
-    bulk_g2s(sm_s + T_L12, tb_ + L.lut12, 4 * FB_SIZE, bar);
+    bulk_g2s(sm_s + T_C12, tb_ + L.clut12, 2 * FB_SIZE, bar);
+    if (a.has_l12) bulk_g2s(sm_s + T_L12, tb_ + L.lut12, 4 * FB_SIZE, bar);
   }
   uint64_t wb_cur = 0, wb_next = 0, wb_nn = 0;
   if (g0 * W + wib < a.nseq) wb_cur = stage_words(a, g0 * W + wib, wbase);
@@ -754,7 +805,8 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
   T.wl = sm_s + T_WL + 16 * (lane & 7);
   T.lim = sm_s + T_LIM;
   T.base = sm_s + T_BASE;
-  T.l12 = sm_s + T_L12;
+  T.l12 = a.has_l12 ? sm_s + T_L12 : 0u;
+  T.c12 = sm_s + T_C12;
   T.t = table_view(a.table, a.max_codes, hdr->ncodes);
   T.kind = hdr->kind;
   MARK(TRACE_SLOTS - 3);
@@ -920,6 +972,311 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) 
 #undef MARK
 }
 
+
+// ---------------------------------------------------------------------------
+// Two-phase fused kernel (default).  One CTA per SM owns a contiguous range of
+// tiles.  Phase 1: its warps count every tile of the range (GAP: boundary +
+// gap byte; SYNC: intra-sequence self-synchronisation and the seam seed, as
+// tile_counts) and record each subsequence's entry and lane prefix plus the
+// tile total in the workspace.  The CTA then scans its tile totals and
+// publishes its aggregate with a decoupled look-back across CTAs (148
+// descriptors, resolved in one round of loads).  Phase 2: the warps decode
+// every tile of the range into shared-memory staging and flush it with
+// coalesced 128-bit stores.  No warp waits for another warp inside a phase,
+// so the memory-bound flushes of some warps overlap the table-bound decoding
+// of others; the count phase needs only the 12-bit count table, so it starts
+// as soon as that table lands.
+// ---------------------------------------------------------------------------
+
+// exclusive prefix of CTA `c` over the epoch-tagged CTA descriptors: every
+// predecessor descriptor is loaded in one round (lane l takes c-1-l, c-33-l..)
+__device__ unsigned long long lookback_wide(unsigned long long* desc, uint64_t c, uint32_t ep) {
+  const uint32_t lane = threadIdx.x & 31;
+  unsigned long long excl = 0;
+  int64_t hi = (int64_t)c - 1;
+  while (hi >= 0) {
+    // up to 4 x 32 predecessors per round
+    unsigned long long d[4];
+    bool ready;
+    do {
+      ready = true;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t idx = hi - (int64_t)lane - 32 * q;
+        d[q] = idx >= 0 ? ld_acquire(desc + idx) : mkdesc(ep, D_INC, 0);
+        ready = ready && desc_ready(d[q], ep);
+      }
+      if (!__all_sync(0xffffffffu, ready)) __nanosleep(32); else break;
+    } while (true);
+    // nearest inclusive descriptor (smallest distance) ends the walk
+    uint32_t stop_q = 4, stop_lane = 32;
+#pragma unroll
+    for (int q = 3; q >= 0; --q) {
+      const unsigned m = __ballot_sync(0xffffffffu, (d[q] & D_INC) != 0);
+      if (m) { stop_q = q; stop_lane = __ffs(m) - 1; }
+    }
+    unsigned long long v = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const bool take = (uint32_t)q < stop_q || ((uint32_t)q == stop_q && lane <= stop_lane);
+      v += take ? (d[q] & D_VAL) : 0ull;
+    }
+    excl += warp_sum(v);
+    if (stop_q < 4) break;
+    hi -= 128;
+  }
+  return excl;
+}
+
+template <int VAR, int TR>
+__global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a) {
+#define MARK(slot)                                                                                  \
+  do {                                                                                              \
+    if (TR && (threadIdx.x & 31) == 0 && (slot) < TRACE_SLOTS)                                      \
+      a.trace[((size_t)blockIdx.x * a.warps + (threadIdx.x >> 5)) * TRACE_SLOTS + (slot)] = gtime(); \
+  } while (0)
+  MARK(0);
+  extern __shared__ __align__(16) unsigned char sm[];
+  // mbarriers: [0] count tables (c12, lim, base), [1] decode tables (wlut8,
+  // lut12), [2] CTA output offset published (1 arrival)
+  __shared__ __align__(8) unsigned long long s_mb[3];
+  __shared__ unsigned long long s_ctaoff;
+  __shared__ uint32_t s_wsum[32];
+  __shared__ uint32_t s_carry;
+  const uint32_t ep = *(volatile const unsigned int*)a.ws_hdr + 1u;
+  const TableHdr* hdr = static_cast<const TableHdr*>(a.table);
+  if (VAR == BH_VARIANT_SYNC && !hdr->complete) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) tag_status(a.rep, ep, NEED_STAGED);
+    fused_finish(a, ep);
+    return;
+  }
+  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  unsigned char* pw = sm + a.tables_bytes + (size_t)wib * a.per_warp_bytes;
+  uint32_t* const wbase = reinterpret_cast<uint32_t*>(pw);
+  const uint32_t wbase_s = smem_u32(pw);
+  const uint32_t stg_s = wbase_s + 8 * a.wpb;  // two word buffers, then staging
+  const uint16_t* stg = reinterpret_cast<const uint16_t*>(pw + 8 * (size_t)a.wpb);
+  const uint32_t W = a.warps;
+  const uint64_t G = gridDim.x, cta = blockIdx.x;
+  const uint64_t t0 = a.nseq * cta / G, t1 = a.nseq * (cta + 1) / G;
+  bool bad = false;
+
+  const uint32_t sm_s = smem_u32(sm);
+  const uint32_t bar_ct = smem_u32(&s_mb[0]), bar_dt = bar_ct + 8, bar_off = bar_ct + 16;
+  if (threadIdx.x == 0) {
+    TableLayout L(a.max_codes);
+    const char* tb_ = static_cast<const char*>(a.table);
+    mbar_init(bar_ct, 1);
+    mbar_init(bar_dt, 1);
+    mbar_init(bar_off, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_expect_tx(bar_ct, 528 + 2 * FB_SIZE);
+    bulk_g2s(sm_s + T_C12, tb_ + L.clut12, 2 * FB_SIZE, bar_ct);
+    bulk_g2s(sm_s + T_LIM, tb_ + L.lim, 528, bar_ct);  // lim, base (contiguous)
+    mbar_expect_tx(bar_dt, 4096 + (a.has_l12 ? 4 * FB_SIZE : 0));
+    bulk_g2s(sm_s + T_WL, tb_ + L.wlut8, 4096, bar_dt);  // entries packed, spread below
+    if (a.has_l12) bulk_g2s(sm_s + T_L12, tb_ + L.lut12, 4 * FB_SIZE, bar_dt);
+  }
+  uint64_t tile = t0 + wib;
+  uint64_t wb_a = 0, wb_b = 0;
+  if (tile < t1) wb_a = stage_words(a, tile, wbase);
+  cp_commit();
+  FTab T;
+  T.wl = sm_s + T_WL + 16 * (lane & 7);
+  T.lim = sm_s + T_LIM;
+  T.base = sm_s + T_BASE;
+  T.l12 = a.has_l12 ? sm_s + T_L12 : 0u;
+  T.c12 = sm_s + T_C12;
+  T.t = table_view(a.table, a.max_codes, hdr->ncodes);
+  T.kind = hdr->kind;
+  __syncthreads();  // barriers initialised
+  mbar_wait(bar_ct, 0);
+  MARK(1);
+
+  // ---- phase 1: count ----------------------------------------------------
+  uint32_t buf = 0;
+  for (; tile < t1; tile += W) {
+    const uint64_t tn = tile + W;
+    if (tn < t1) wb_b = stage_words(a, tn, wbase + (buf ^ 1) * a.wpb);
+    cp_commit();
+    cp_wait<1>();
+    __syncwarp();
+    const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
+    uint32_t e, c;
+    tile_counts<VAR>(a, T, tile, wbase_s + 4 * a.wpb * buf, wb_a, nsl, ep, e, c, bad);
+    uint32_t incl = c;
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      if ((int)lane >= off) incl += y;
+    }
+    const uint32_t b = (uint32_t)((tile * a.sps + lane) * a.sb - wb_a);
+    const uint32_t de = e - b;
+    if (de > 0xffffu || incl > 0xffffu) bad = true;
+    a.lane_info[tile * 32 + lane] = (de & 0xffffu) | ((incl - c) << 16);
+    if (lane == 31) a.tile_cnt[tile] = incl;
+    wb_a = wb_b;
+    buf ^= 1;
+  }
+  MARK(2);
+
+  // ---- CTA scan of the tile totals, decode tables spread -----------------
+  mbar_wait(bar_dt, 0);
+  // spread wlut8 into its 8 replicas ([entry][replica] uint4), highest entries
+  // first: entry e's replicas overwrite packed entries >= e only.  The
+  // barriers also make the range's tile totals visible to the scan below.
+  for (int hi = 255; hi >= 0; hi -= (int)blockDim.x) {
+    const int e = hi - (int)threadIdx.x;
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (e >= 0) v = lds128(sm_s + T_WL + 16 * e);
+    __syncthreads();
+    if (e >= 0)
+      for (uint32_t r = 0; r < 8; ++r) sts128(sm_s + T_WL + 128 * e + 16 * r, v);
+    __syncthreads();
+  }
+  const uint32_t nt = (uint32_t)(t1 - t0);
+  const uint32_t nw = blockDim.x >> 5;
+  uint32_t carry = 0;
+  for (uint32_t base = 0; base < nt; base += blockDim.x) {
+    const uint32_t i = base + threadIdx.x;
+    const uint32_t v = i < nt ? a.tile_cnt[t0 + i] : 0u;
+    uint32_t incl = v;
+    for (int off = 1; off < 32; off <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+      if ((int)lane >= off) incl += y;
+    }
+    if (lane == 31) s_wsum[wib] = incl;
+    __syncthreads();
+    if (wib == 0) {
+      const uint32_t ws = lane < nw ? s_wsum[lane] : 0u;
+      uint32_t wi = ws;
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, wi, off);
+        if ((int)lane >= off) wi += y;
+      }
+      if (lane < nw) s_wsum[lane] = wi - ws;
+      if (lane == 31) s_carry = wi;
+    }
+    __syncthreads();
+    if (i < nt) a.tile_off[t0 + i] = carry + s_wsum[wib] + incl - v;
+    carry += s_carry;
+    __syncthreads();
+  }
+  // warp 0 publishes the CTA aggregate and looks back; the others start decoding
+  if (wib == 0) {
+    unsigned long long excl = 0;
+    if (cta == 0) {
+      if (lane == 0) st_release(a.cnt_desc, mkdesc(ep, D_INC, carry));
+    } else {
+      if (lane == 0) st_release(a.cnt_desc + cta, mkdesc(ep, D_AGG, carry));
+      excl = lookback_wide(a.cnt_desc, cta, ep);
+      if (lane == 0) st_release(a.cnt_desc + cta, mkdesc(ep, D_INC, excl + carry));
+    }
+    if (lane == 0) {
+      s_ctaoff = excl;
+      if (cta == G - 1) {
+        a.rep->total_symbols = excl + carry;
+        if (excl + carry != a.nsym) tag_status(a.rep, ep, VAR == BH_VARIANT_GAP ? BH_BADGAP : BH_TRUNCATED);
+      }
+      mbar_arrive(bar_off);
+    }
+  }
+  MARK(3);
+
+  // ---- phase 2: decode and write -----------------------------------------
+  tile = t0 + wib;
+  buf = 0;
+  if (tile < t1) wb_a = stage_words(a, tile, wbase);
+  cp_commit();
+  bool have_off = false;
+  unsigned long long Pc = 0;
+  for (; tile < t1; tile += W) {
+    const uint64_t tn = tile + W;
+    if (tn < t1) wb_b = stage_words(a, tn, wbase + (buf ^ 1) * a.wpb);
+    cp_commit();
+    const uint32_t info = a.lane_info[tile * 32 + lane];
+    const uint32_t C = a.tile_cnt[tile];
+    const uint32_t toff = a.tile_off[tile];
+    cp_wait<1>();
+    __syncwarp();
+    const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
+    const uint32_t base_s = wbase_s + 4 * a.wpb * buf;
+    const uint32_t b = (uint32_t)((tile * a.sps + lane) * a.sb - wb_a);
+    const uint32_t e = b + (info & 0xffffu);
+    const uint32_t o = info >> 16;
+    const uint32_t on = __shfl_down_sync(0xffffffffu, o, 1);
+    const uint32_t c = lane < nsl ? (lane == 31 ? C : on) - o : 0u;
+    if (!have_off) {
+      have_off = __shfl_sync(0xffffffffu, lane == 0 ? mbar_test(bar_off, 0) : 0u, 0) != 0;
+      if (have_off) Pc = *(volatile unsigned long long*)&s_ctaoff;
+    }
+    const bool fits = C + 16 <= a.cap;
+    const uint32_t sh = have_off ? (uint32_t)(Pc + toff) & 7u : 0u;
+    if (fits && c) {
+      SR r;
+      r.init(base_s, e);
+      if (!fdecode(r, c, stg_s + 2 * (sh + o), T)) bad = true;
+    }
+    __syncwarp();
+    const bool aligned = have_off;
+    if (!have_off) {
+      mbar_wait(bar_off, 0);
+      Pc = *(volatile unsigned long long*)&s_ctaoff;
+      have_off = true;
+    }
+    const unsigned long long P = Pc + toff;
+    if (fits) {
+      if (aligned) flush_aligned_stg(a.out, a.nsym, P, C, stg_s);
+      else flush_compact(a.out, a.nsym, P, C, stg_s);
+    } else {
+      // reference rounds (staging.py:123-146) with capacity cap - 8
+      const bool active = lane < nsl;
+      const uint32_t capw = a.cap - 8;
+      const uint32_t endl = o + c;
+      uint32_t si = 0;
+      while (si < C) {
+        const uint32_t window = si + capw;
+        const unsigned mj = __ballot_sync(0xffffffffu, active && endl > si);
+        const uint32_t jl = __ffs(mj) - 1;
+        const unsigned mk = __ballot_sync(0xffffffffu, active && lane >= jl && endl > window);
+        const uint32_t kl = mk ? __ffs(mk) - 1 : nsl;
+        if (kl == jl) {
+          if (lane == jl) {
+            SR r;
+            r.init(base_s, e);
+            if (!fdecode_global(r, c, a.out, P + o, a.nsym, T)) bad = true;
+          }
+          si = __shfl_sync(0xffffffffu, endl, jl);
+          continue;
+        }
+        const uint32_t temp_end = kl < nsl ? __shfl_sync(0xffffffffu, o, kl & 31) : C;
+        const uint64_t g0w = P + si;
+        const uint64_t gbase = g0w & ~7ull;
+        const bool mine = lane >= jl && lane < kl && c;
+        const uint32_t d = stg_s + 2 * (uint32_t)(P + o - gbase);
+        if (mine) {
+          SR r;
+          r.init(base_s, e);
+          if (!fdecode(r, c, d, T)) bad = true;
+        }
+        __syncwarp();
+        flush_aligned(a.out, a.nsym, g0w, temp_end - si, stg);
+        __syncwarp();
+        si = temp_end;
+      }
+    }
+    __syncwarp();
+    wb_a = wb_b;
+    buf ^= 1;
+  }
+  cp_wait<0>();
+  if (!have_off) mbar_wait(bar_off, 0);  // keep warp 0's arrival inside the CTA's lifetime
+  if (__any_sync(0xffffffffu, bad) && lane == 0) tag_status(a.rep, ep, BH_INVALID);
+  MARK(TRACE_SLOTS - 2);
+  fused_finish(a, ep);
+  MARK(TRACE_SLOTS - 1);
+#undef MARK
+}
+
 }  // namespace bh
 
 // ---------------------------------------------------------------------------
@@ -937,10 +1294,10 @@ int env_int(const char* name, int dflt) {
 }
 
 struct FusedCfg {
-  uint32_t warps, cap, wpb, per_warp, tables, smem;
+  uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12, two_phase;
 };
 
-FusedCfg fused_cfg(const bh_stream* s) {
+FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   FusedCfg c;
   const uint32_t seq_bits = s->subseq_bits * s->subseqs_per_seq;
   // words one tile can stage: its span (+1 for a straddle), the 16-byte
@@ -956,8 +1313,11 @@ FusedCfg fused_cfg(const bh_stream* s) {
   if (cap > cmax) cap = cmax;
   if (cap < 64) cap = 64;
   c.cap = (cap + 7) & ~7u;
-  c.tables = (uint32_t)align16(T_END);
-  c.per_warp = (uint32_t)align16(12 * (size_t)c.wpb + 2 * (size_t)c.cap + 32);
+  c.has_l12 = !(tune && tune->max_len && tune->max_len <= 8);
+  c.two_phase = env_int("BH_FUSED_V", 2) != 1;
+  c.tables = (uint32_t)align16(c.has_l12 ? T_END : T_END_NOL12);
+  // word buffers (two for the two-phase kernel, three for the group pipeline), staging
+  c.per_warp = (uint32_t)align16((c.two_phase ? 8 : 12) * (size_t)c.wpb + 2 * (size_t)c.cap + 32);
   int w = env_int("BH_FUSED_WARPS", 0);
   if (w <= 0) {
     w = (int)((220 * 1024 - c.tables) / c.per_warp);
@@ -994,8 +1354,8 @@ extern "C" int bh_debug_fused_trace(void* trace_dev) {
   return BH_OK;
 }
 
-extern "C" int bh_debug_fused_shape(const bh_stream* s, uint32_t* warps, uint32_t* smem) {
-  FusedCfg c = fused_cfg(s);
+extern "C" int bh_debug_fused_shape(const bh_stream* s, const bh_tune* tune, uint32_t* warps, uint32_t* smem) {
+  FusedCfg c = fused_cfg(s, tune);
   if (warps) *warps = c.warps;
   if (smem) *smem = c.smem;
   return BH_OK;
@@ -1013,8 +1373,9 @@ extern "C" int bh_fused_supported(const bh_stream* s, int variant) {
 }
 
 // workspace: [64 B header: epoch, CTA-done counter][cnt desc][exit desc]
+//            [lane info u32 x 32 per tile][tile count u32][tile offset u32]
 extern "C" size_t bh_fused_workspace_bytes(const bh_stream* s, int, const bh_tune*) {
-  return 64 + 16 * nseq_of(s) + 256;
+  return 64 + 16 * nseq_of(s) + 4 * 34 * nseq_of(s) + 256;
 }
 
 extern "C" int bh_workspace_reset(void* ws, size_t bytes, void* cuda_stream) {
@@ -1027,7 +1388,7 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   (void)tune;
   const uint64_t nseq = nseq_of(s);
   if (ws_bytes < bh_fused_workspace_bytes(s, variant, tune)) return BH_BAD_ARGUMENT;
-  FusedCfg cfg = fused_cfg(s);
+  FusedCfg cfg = fused_cfg(s, tune);
   FusedArgs a;
   a.words = s->words_dev;
   a.words_alloc = (((s->total_bits + 31) / 32 + BH_WORD_PAD) & ~3ull);
@@ -1045,12 +1406,16 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.ws_hdr = static_cast<unsigned int*>(ws);
   a.cnt_desc = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + 64);
   a.exit_desc = a.cnt_desc + nseq;
+  a.lane_info = reinterpret_cast<uint32_t*>(a.exit_desc + nseq);
+  a.tile_cnt = a.lane_info + 32 * nseq;
+  a.tile_off = a.tile_cnt + nseq;
   a.rep = static_cast<DevReport*>(report_dev);
   a.wpb = cfg.wpb;
   a.cap = cfg.cap;
   a.warps = cfg.warps;
   a.per_warp_bytes = cfg.per_warp;
   a.tables_bytes = cfg.tables;
+  a.has_l12 = cfg.has_l12;
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -1058,8 +1423,13 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   a.trace = g_trace;
-  const void* fn = variant == BH_VARIANT_GAP ? (g_trace ? (const void*)k_fused<BH_VARIANT_GAP, 1> : (const void*)k_fused<BH_VARIANT_GAP, 0>)
-                                             : (g_trace ? (const void*)k_fused<BH_VARIANT_SYNC, 1> : (const void*)k_fused<BH_VARIANT_SYNC, 0>);
+  const void* fn;
+  if (cfg.two_phase)
+    fn = variant == BH_VARIANT_GAP ? (g_trace ? (const void*)k_fused2<BH_VARIANT_GAP, 1> : (const void*)k_fused2<BH_VARIANT_GAP, 0>)
+                                   : (g_trace ? (const void*)k_fused2<BH_VARIANT_SYNC, 1> : (const void*)k_fused2<BH_VARIANT_SYNC, 0>);
+  else
+    fn = variant == BH_VARIANT_GAP ? (g_trace ? (const void*)k_fused<BH_VARIANT_GAP, 1> : (const void*)k_fused<BH_VARIANT_GAP, 0>)
+                                   : (g_trace ? (const void*)k_fused<BH_VARIANT_SYNC, 1> : (const void*)k_fused<BH_VARIANT_SYNC, 0>);
   // launch attributes and occupancy cached per (kernel, threads, smem)
   static std::mutex mu;
   static std::map<std::tuple<const void*, uint32_t, uint32_t>, int> occ;

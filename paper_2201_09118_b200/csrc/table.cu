@@ -205,9 +205,27 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
   uint32_t* dlut8 = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(blob) + L.dlut8);
   uint8_t* clut8 = reinterpret_cast<uint8_t*>(reinterpret_cast<char*>(blob) + L.clut8);
   uint32_t* lut12 = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(blob) + L.lut12);
+  uint16_t* clut12 = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(blob) + L.clut12);
+  __syncthreads();  // s_lut is reused for the 12-bit codes below
+  uint16_t* s_len12 = reinterpret_cast<uint16_t*>(s_lut);  // 4096 lengths (8 KB)
   for (int v = threadIdx.x; v < FB_SIZE; v += blockDim.x) {
     uint32_t e = slow_lookup(t, (uint32_t)v << (32 - FB));
-    lut12[v] = ((e >> 16) & 0xff) <= (uint32_t)FB ? e : 0u;
+    const uint32_t len = (e >> 16) & 0xff;
+    lut12[v] = len <= (uint32_t)FB ? e : 0u;
+    s_len12[v] = (uint16_t)(len <= (uint32_t)FB ? len : 0u);
+  }
+  __syncthreads();
+  // count table: every whole codeword of the 12-bit window (zero fill past the
+  // window cannot change a match of a codeword that lies inside it)
+  for (int v = threadIdx.x; v < FB_SIZE; v += blockDim.x) {
+    uint32_t pos = 0, starts = 0;
+    while (pos < (uint32_t)FB) {
+      const uint32_t len = s_len12[((uint32_t)v << pos) & (FB_SIZE - 1)];
+      if (len == 0 || pos + len > (uint32_t)FB) break;
+      starts |= 1u << pos;
+      pos += len;
+    }
+    clut12[v] = (uint16_t)(starts | (pos << 12));
   }
   for (int v = threadIdx.x; v < 256; v += blockDim.x) {
     uint32_t e = slow_lookup(t, (uint32_t)v << 24);

@@ -6,6 +6,7 @@ Records globaltimer stamps at the pipeline's phase boundaries for every warp
 (bh_debug_fused_trace) and prints where a CTA's time goes.
 """
 import argparse
+import os
 import ctypes as C
 import sys
 from pathlib import Path
@@ -30,9 +31,9 @@ def main():
     dec = Decoder(stream, args.variant)
     lib = dec.lib
     lib.bh_debug_fused_trace.argtypes = [C.c_void_p]
-    lib.bh_debug_fused_shape.argtypes = [C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+    lib.bh_debug_fused_shape.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
     W, sm = C.c_uint32(), C.c_uint32()
-    lib.bh_debug_fused_shape(dec.ds.ref, C.byref(W), C.byref(sm))
+    lib.bh_debug_fused_shape(dec.ds.ref, C.byref(dec.tune), C.byref(W), C.byref(sm))
     W = W.value
     nmax = 148 * 8 * W
     tr = torch.zeros(nmax * SLOTS, dtype=torch.int64, device="cuda")
@@ -63,6 +64,17 @@ def main():
         x = x[x >= 0]
         return f"med {np.median(x) / 1e3:6.2f} p90 {np.percentile(x, 90) / 1e3:6.2f} max {x.max() / 1e3:6.2f}" if len(x) else "-"
 
+    if os.environ.get("BH_FUSED_V", "2") != "1":
+        print("start            ", q(rel[:, 0]))
+        print("count tables in  ", q(rel[:, 1]))
+        print("count phase done ", q(rel[:, 2]))
+        print("scan+publish     ", q(rel[:, 3]))
+        print("decode phase done", q(rel[:, SLOTS - 2]))
+        print("finish           ", q(rel[:, SLOTS - 1]))
+        cta_end = rel[:, SLOTS - 1].reshape(ncta, W).max(1)
+        print("CTA end          ", q(cta_end))
+        np.save("gpurun_out/trace_%s_%s.npy" % (args.config, args.variant), rel)
+        return
     print("start            ", q(rel[:, 0]))
     print("barrier init     ", q(rel[:, SLOTS - 5]))
     print("bulk tables in   ", q(rel[:, SLOTS - 4]))
