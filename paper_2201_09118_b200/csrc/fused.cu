@@ -1,36 +1,38 @@
-// fused.cu -- single-pass fused decoders: the bh_decode fast path.
+// fused.cu -- the fused decoders: the bh_decode fast path (one kernel per decode).
 //
-// One kernel per decode.  A persistent grid of warps walks the sequences
-// (tiles) in order; per tile, one lane per subsequence:
+// k_fused2 runs one persistent CTA per SM; CTA c owns a contiguous range of
+// tiles (a tile = one sequence = `subseqs_per_seq` subsequences, one lane per
+// subsequence).  Two phases:
 //
-//   1. the tile's compressed words are cp.async-staged into shared memory one
-//      tile ahead (double buffer per warp);
-//   2. entries: GAP  -- boundary + gap byte (gap_decoder.py:24-33);
-//               SYNC -- intra-sequence self-synchronisation (sync_decoder.py
-//                       :62-109): every lane decodes its window from the
-//                       boundary, then exits are handed right with shuffles and
-//                       re-decoded until a ballot shows no live chain.  A
-//                       re-decode walks the old and the new decode in lock-step
-//                       and stops as soon as they meet (self-synchronisation),
-//                       reusing the old tail.  The seam to the previous sequence
-//                       (inter_sync, :116-149) is resolved in the same pass:
-//                       the 32 possible seeds of the first slot are tried in
-//                       parallel (lane o = boundary + o), so a sequence whose
-//                       exit is seed-independent publishes it immediately and
-//                       the true seed only selects the first slot's count;
-//   3. counts: 12-bit multi-codeword count table, warp scan, decoupled
-//      look-back over per-tile descriptors (state.py:44-53 output_index);
-//   4. decode-and-write (staging.py:113-147): lanes decode in lock-step, two
-//      symbols per step, into per-lane shared-memory rows whose odd word
-//      stride puts every lane in its own bank; the warp then gathers the rows
-//      into output order with 128-bit loads and flushes with coalesced
-//      128-bit stores.  A row holds the largest possible subsequence output,
-//      so the whole tile is always staged (the reference's capacity rounds
-//      only matter for its DecodeStats, which the staged pipeline reproduces).
-//
-// Shared-memory bank conflicts are designed out: the 8-bit decode and count
-// tables are replicated per lane (lane l reads only bank l), staging writes are
-// bank-private, and the gather reads 16-byte-aligned consecutive chunks.
+//   phase 1 (count): each warp takes tiles of the range round-robin, stages
+//     the tile's words with cp.async (double buffer) and computes every
+//     lane's entry and codeword count --
+//       GAP  -- boundary + gap byte (gap_decoder.py:24-33), count over the
+//               window to the next entry (gap_decoder.py:36-68);
+//       SYNC -- intra-sequence self-synchronisation (sync_decoder.py:62-109):
+//               every lane decodes its window from the boundary, exits are
+//               handed right with shuffles and re-decoded until a ballot shows
+//               no live chain (a re-decode walks the old and new decode in
+//               lock-step and stops where they meet).  The seam to the
+//               previous sequence (inter_sync, :116-149) is resolved in the
+//               same pass: the 32 possible seeds of the first slot are tried in
+//               parallel, so a sequence whose exit is seed-independent
+//               publishes it at once (epoch-tagged per-tile exit descriptors).
+//     Counting uses a 12-bit start-mask table: one lookup covers every whole
+//     codeword of the next 12 bits (popcount), and the lookup that crosses
+//     the window end counts the starts below it.  The entry offset and the
+//     lane's prefix go to the workspace, the tile total to shared memory.
+//   between the phases: one CTA barrier; each warp sums the totals before its
+//     tiles itself; warp 0 publishes the CTA aggregate and resolves the CTA's
+//     output offset with a decoupled look-back over the CTA descriptors
+//     (state.py:44-53 output_index), while the other warps already decode.
+//   phase 2 (decode and write, staging.py:113-147): lanes decode in lock-step
+//     through an 8-bit multi-symbol table (up to six codewords per lookup,
+//     replicated eight ways so a quarter-warp never conflicts) into compact
+//     shared-memory staging with one halfword and three aligned word stores
+//     per lookup; the warp then flushes the tile with coalesced 128-bit
+//     stores (staging aligned to the output once the offset is known).  A
+//     tile larger than the staging capacity takes the reference's rounds.
 //
 // No memory needs resetting between calls: descriptors and the report are
 // tagged with a per-call epoch (bh_workspace_reset once per allocation).
@@ -93,7 +95,8 @@ constexpr uint32_t T_WL = 0;                      // uint4 [256][8] replicated w
 constexpr uint32_t T_LIM = T_WL + 256 * 8 * 16;   // u64 [33]
 constexpr uint32_t T_BASE = T_LIM + 33 * 8;       // i64 [33]
 constexpr uint32_t T_C12 = T_BASE + 33 * 8;       // u16 [4096] 12-bit count table
-constexpr uint32_t T_L12 = T_C12 + 2 * FB_SIZE;   // u32 [4096] second level: codes of 9..12 bits (optional)
+constexpr uint32_t T_WP = T_C12 + 2 * FB_SIZE;    // uint4 [256] packed wlut8 (bulk-copy target)
+constexpr uint32_t T_L12 = T_WP + 4096;           // u32 [4096] second level: codes of 9..12 bits (optional)
 constexpr uint32_t T_END_NOL12 = T_L12;
 constexpr uint32_t T_END = T_L12 + 4 * FB_SIZE;
 
@@ -128,6 +131,9 @@ __device__ __forceinline__ uint32_t lds8(uint32_t a) {
   unsigned short v;
   asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(a) : "memory");
   return v;
+}
+__device__ __forceinline__ void sts32(uint32_t a, uint32_t v) {
+  asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v) : "memory");
 }
 __device__ __forceinline__ void sts16(uint32_t a, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"((unsigned short)v) : "memory");
@@ -171,8 +177,8 @@ struct SR {
     const uint32_t adv = t >> 5;
     w0 = adv ? w1 : w0;
     w1 = adv ? w2 : w1;
-    w2 = lds32_if(wa, adv, w2);
     wa += adv << 2;
+    w2 = lds32(wa - 4);  // the word after w1 (unchanged when adv == 0): no branch
     off = t & 31;
   }
 };
@@ -280,17 +286,23 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
 __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const FTab& T) {
   const uint32_t wl = pin(T.wl);
   int32_t k = (int32_t)c;
-#ifndef BH_FDEC_PRED
-  while (k >= 6) {
+#if !defined(BH_FDEC_PRED)
+  while (k >= 7) {
     const uint32_t win = r.peek();
     const uint4 w = lds128(wl + ((win >> 24) << 7));
     if (w.w) {
+      // one halfword store, then three aligned word stores: an odd start
+      // shifts the entry by one halfword (the seventh halfword written is
+      // garbage inside the lane's own range, overwritten by its next store)
+      const uint32_t odd = dst & 2u;
+      const uint32_t sel = odd ? 0x5432u : 0x3210u;
+      const uint32_t a4 = (dst & ~3u) + (odd << 1);
+#ifndef BH_X_NOSTORE
       sts16(dst, w.x);
-      sts16(dst + 2, w.x >> 16);
-      sts16(dst + 4, w.y);
-      sts16(dst + 6, w.y >> 16);
-      sts16(dst + 8, w.z);
-      sts16(dst + 10, w.z >> 16);
+      sts32(a4, __byte_perm(w.x, w.y, sel));
+      sts32(a4 + 4, __byte_perm(w.y, w.z, sel));
+      sts32(a4 + 8, __byte_perm(w.z, w.z, sel));
+#endif
       const int32_t n = (int32_t)((w.w >> 4) & 15u);
       dst += (uint32_t)n << 1;
       k -= n;
@@ -334,18 +346,6 @@ __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const F
   return true;
 }
 
-// re-store the first min(c, 2) symbols of a lane's range (after __syncwarp)
-__device__ __forceinline__ void fix_first2(uint32_t base_s, uint32_t e, uint32_t c, uint32_t dst, const FTab& T) {
-  SR r;
-  r.init(base_s, e);
-  const uint32_t m = c < 2 ? c : 2;
-  for (uint32_t i = 0; i < m; ++i) {
-    const uint32_t s = fone(r.peek(), T);
-    sts16(dst + 2 * i, s);
-    r.skip((s >> 16) & 0xffu);
-  }
-}
-
 // bypass: decode straight to global memory (rare; guarded by the output size)
 __device__ bool fdecode_global(SR& r, uint32_t c, uint16_t* out, uint64_t at, uint64_t nsym, const FTab& T) {
   for (uint32_t k = 0; k < c; ++k) {
@@ -383,31 +383,6 @@ __device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co
       ++nn;
     }
   }
-}
-
-// warp look-back over epoch-tagged descriptors (32 predecessors per step)
-__device__ __forceinline__ unsigned long long lookback(unsigned long long* desc, uint64_t tile, uint32_t ep) {
-  const uint32_t lane = threadIdx.x & 31;
-  unsigned long long excl = 0;
-  int64_t base = (int64_t)tile - 1;
-  while (base >= 0) {
-    const int64_t idx = base - (int64_t)lane;
-    const bool valid = idx >= 0;
-    unsigned long long d;
-    while (true) {
-      d = valid ? ld_acquire(desc + idx) : 0ull;
-      const bool ready = !valid || desc_ready(d, ep);
-      if (__all_sync(0xffffffffu, ready)) break;
-      __nanosleep(20);
-    }
-    const unsigned inc = __ballot_sync(0xffffffffu, valid && (d & D_INC));
-    const int stop_lane = inc ? __ffs(inc) - 1 : 31;
-    const unsigned long long v = (valid && (int)lane <= stop_lane) ? (d & D_VAL) : 0ull;
-    excl += warp_sum(v);
-    if (inc) break;
-    base -= 32;
-  }
-  return excl;
 }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
@@ -704,13 +679,6 @@ __device__ __forceinline__ void fused_finish(const FusedArgs& a, uint32_t ep) {
   }
 }
 
-// One CTA processes a group of `warps` consecutive tiles per iteration (warp w
-// takes tile group*warps + w).  Software pipeline, per iteration k:
-//   count the tile of group k+1 (words staged one iteration ahead),
-//   decode the tile of group k into staging,
-//   warp 0: look back for group k+1's output offset (a full iteration early),
-//   flush the tile of group k once group k's offset is published.
-// So the look-back latency never stalls the decode in steady state.
 // debug timeline: per warp, TRACE_SLOTS globaltimer stamps (bh_debug_fused_trace)
 constexpr int TRACE_SLOTS = 64;
 __device__ __forceinline__ unsigned long long gtime() {
@@ -719,258 +687,7 @@ __device__ __forceinline__ unsigned long long gtime() {
   return t;
 }
 
-template <int VAR, int TR>
-__global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused(const FusedArgs a) {
-#define MARK(slot)                                                                                  \
-  do {                                                                                              \
-    if (TR && (threadIdx.x & 31) == 0 && (slot) < TRACE_SLOTS)                                      \
-      a.trace[((size_t)blockIdx.x * a.warps + (threadIdx.x >> 5)) * TRACE_SLOTS + (slot)] = gtime(); \
-  } while (0)
-  MARK(0);
-  extern __shared__ __align__(16) unsigned char sm[];
-  __shared__ uint32_t s_C[2][32];
-  __shared__ unsigned long long s_Pw[2][32];
-  // mbarriers: [0] tables; [1+p] counts of this CTA's groups of parity p
-  // (W arrivals); [3+p] offsets of those groups published (1 arrival).  Group
-  // #m of the CTA uses parity p = m & 1 and phase (m >> 1) & 1: a warp can run
-  // at most one group ahead, so no barrier is ever two phases ahead of a waiter.
-  __shared__ __align__(8) unsigned long long s_mb[5];
-  // Per-call epoch kept on the device (graph-replayable): every CTA reads the
-  // epoch of the last completed call; the last CTA of this call to finish
-  // advances it (fused_finish), so all CTAs of one call agree.
-  const uint32_t ep = *(volatile const unsigned int*)a.ws_hdr + 1u;
-  const TableHdr* hdr = static_cast<const TableHdr*>(a.table);
-  if (VAR == BH_VARIANT_SYNC && !hdr->complete) {
-    // the speculative windows differ from the reference's: only complete books
-    // (where no window can fail) may take the fused path
-    if (blockIdx.x == 0 && threadIdx.x == 0) tag_status(a.rep, ep, NEED_STAGED);
-    fused_finish(a, ep);
-    return;
-  }
-  const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  unsigned char* pw = sm + a.tables_bytes + (size_t)wib * a.per_warp_bytes;
-  uint32_t* const wbase = reinterpret_cast<uint32_t*>(pw);
-  const uint32_t wbase_s = smem_u32(pw);
-  const uint32_t stg_s = wbase_s + 12 * a.wpb;  // three word buffers, then staging
-  const uint16_t* stg = reinterpret_cast<const uint16_t*>(pw + 12 * (size_t)a.wpb);
-  const uint32_t W = a.warps;
-  const uint64_t ngroups = (a.nseq + W - 1) / W;
-  const uint64_t G = gridDim.x;
-  const uint64_t g0 = blockIdx.x;  // grid <= ngroups
-  bool bad = false;
 
-  // The tables arrive by three bulk (TMA) copies -- one L2 request per line
-  // per CTA, where 148 CTAs x 8 replica loads of the same lines would queue on
-  // a few L2 slices -- while every warp's words for groups g0 and g0+G are in
-  // flight on cp.async.
-  const uint32_t sm_s = smem_u32(sm);
-  const uint32_t bar = smem_u32(&s_mb[0]);
-  const uint32_t bar_arr = bar + 8, bar_pub = bar + 24;  // + 8 * parity
-  if (threadIdx.x == 0) {
-    TableLayout L(a.max_codes);
-    const char* tb_ = static_cast<const char*>(a.table);
-    mbar_init(bar, 1);
-    mbar_init(bar_arr, W);
-    mbar_init(bar_arr + 8, W);
-    mbar_init(bar_pub, 1);
-    mbar_init(bar_pub + 8, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(bar, 4096 + 528 + 2 * FB_SIZE + (a.has_l12 ? 4 * FB_SIZE : 0));
-    bulk_g2s(sm_s + T_WL, tb_ + L.wlut8, 4096, bar);  // entries packed, spread below
-    bulk_g2s(sm_s + T_LIM, tb_ + L.lim, 528, bar);    // lim, base (contiguous)
-    bulk_g2s(sm_s + T_C12, tb_ + L.clut12, 2 * FB_SIZE, bar);
-    if (a.has_l12) bulk_g2s(sm_s + T_L12, tb_ + L.lut12, 4 * FB_SIZE, bar);
-  }
-  uint64_t wb_cur = 0, wb_next = 0, wb_nn = 0;
-  if (g0 * W + wib < a.nseq) wb_cur = stage_words(a, g0 * W + wib, wbase);
-  cp_commit();
-  if ((g0 + G) * W + wib < a.nseq) wb_next = stage_words(a, (g0 + G) * W + wib, wbase + a.wpb);
-  cp_commit();
-  __syncthreads();  // barrier initialised
-  MARK(TRACE_SLOTS - 5);
-  mbar_wait(bar, 0);
-  MARK(TRACE_SLOTS - 4);
-  // spread wlut8 into its 8 replicas ([entry][replica] uint4), highest entries
-  // first: entry e's replicas overwrite packed entries >= e only
-  for (int hi = 255; hi >= 0; hi -= (int)blockDim.x) {
-    const int e = hi - (int)threadIdx.x;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (e >= 0) v = lds128(sm_s + T_WL + 16 * e);
-    __syncthreads();
-    if (e >= 0)
-      for (uint32_t r = 0; r < 8; ++r) sts128(sm_s + T_WL + 128 * e + 16 * r, v);
-    __syncthreads();
-  }
-  FTab T;
-  T.wl = sm_s + T_WL + 16 * (lane & 7);
-  T.lim = sm_s + T_LIM;
-  T.base = sm_s + T_BASE;
-  T.l12 = a.has_l12 ? sm_s + T_L12 : 0u;
-  T.c12 = sm_s + T_C12;
-  T.t = table_view(a.table, a.max_codes, hdr->ncodes);
-  T.kind = hdr->kind;
-  MARK(TRACE_SLOTS - 3);
-  cp_wait<1>();  // group g0's words
-  __syncthreads();
-  MARK(1);
-
-  // warp 0: wait for every warp's count of group `g` (arrivals are counted per
-  // group parity: a fast warp can run at most one group ahead), look back,
-  // publish per-warp output offsets into s_Pw[par].
-  auto publish = [&](uint64_t g, uint32_t m) {  // group #m of this CTA
-    const uint32_t par = m & 1;
-    mbar_wait(bar_arr + 8 * par, (m >> 1) & 1);
-    const uint32_t v = lane < W ? *(volatile uint32_t*)&s_C[par][lane] : 0u;
-    uint32_t pre = v;
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, pre, off);
-      if ((int)lane >= off) pre += y;
-    }
-    const unsigned long long A = __shfl_sync(0xffffffffu, pre, 31);
-    unsigned long long Pg = 0;
-    if (g == 0) {
-      if (lane == 0) st_release(a.cnt_desc, mkdesc(ep, D_INC, A));
-    } else {
-      if (lane == 0) st_release(a.cnt_desc + g, mkdesc(ep, D_AGG, A));
-      Pg = lookback(a.cnt_desc, g, ep);
-      if (lane == 0) st_release(a.cnt_desc + g, mkdesc(ep, D_INC, Pg + A));
-    }
-    if (lane < W) s_Pw[par][lane] = Pg + (pre - v);
-    if (lane == 0 && g == ngroups - 1) {
-      a.rep->total_symbols = Pg + A;
-      if (Pg + A != a.nsym) tag_status(a.rep, ep, VAR == BH_VARIANT_GAP ? BH_BADGAP : BH_TRUNCATED);
-    }
-    __threadfence_block();
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bar_pub + 8 * par);
-  };
-
-  // per-tile state kept across the pipeline
-  struct TileState { uint32_t e, c, o, C, nsl; uint64_t wb0; };
-  auto count_tile = [&](uint64_t tile, uint32_t buf, uint64_t wb0, uint32_t par) -> TileState {
-    TileState s;
-    s.wb0 = wb0;
-    s.e = 0;
-    s.c = 0;
-    s.nsl = 0;
-    if (tile < a.nseq) {
-      s.nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
-      tile_counts<VAR>(a, T, tile, wbase_s + 4 * a.wpb * buf, wb0, s.nsl, ep, s.e, s.c, bad);
-    }
-    uint32_t incl = s.c;
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-      if ((int)lane >= off) incl += y;
-    }
-    s.C = __shfl_sync(0xffffffffu, incl, 31);
-    s.o = incl - s.c;
-    if (lane == 0) {
-      s_C[par][wib] = s.C;
-      mbar_arrive(bar_arr + 8 * par);  // release: s_C visible to the publisher
-    }
-    return s;
-  };
-
-  // prologue: count g0, publish its offsets
-  TileState cur = count_tile(g0 * W + wib, 0, wb_cur, 0);
-  MARK(2);
-  if (wib == 0) publish(g0, 0);
-  MARK(3);
-
-  uint32_t k = 0, bcur = 0, bnext = 1, bnn = 2;
-  for (uint64_t g = g0; g < ngroups; g += G, ++k) {
-    const uint32_t par = k & 1;
-    const uint64_t gn = g + G, gnn = g + 2 * G;
-    const uint64_t tile = g * W + wib;
-    if (gnn * W + wib < a.nseq) wb_nn = stage_words(a, gnn * W + wib, wbase + bnn * a.wpb);
-    cp_commit();
-    cp_wait<1>();  // buffers of groups g and g+G have landed
-    __syncwarp();
-    const uint32_t base_s = wbase_s + 4 * a.wpb * bcur;
-    const bool have = tile < a.nseq;
-    const bool fits = cur.C + 16 <= a.cap;
-    TileState nxt = cur;
-    uint32_t sh = 0, aligned = 0;  // staging aligned to the output (offsets already published)
-    // count the next group's tile, then decode this group's tile into
-    // staging aligned to its output (the group's offsets were published an
-    // iteration ago; wait only if they are not there yet)
-    if (gn < ngroups) nxt = count_tile(gn * W + wib, bnext, wb_next, par ^ 1);
-    MARK(4 + 5 * k);
-    const uint32_t ready = __shfl_sync(0xffffffffu, lane == 0 ? mbar_test(bar_pub + 8 * par, (k >> 1) & 1) : 0u, 0);
-    if (ready) sh = (uint32_t)(*(volatile unsigned long long*)&s_Pw[par][wib]) & 7u;
-    if (have && fits && cur.c) {
-      SR r;
-      r.init(base_s, cur.e);
-      if (!fdecode(r, cur.c, stg_s + 2 * ((ready ? sh : 0u) + cur.o), T)) bad = true;
-    }
-    aligned = ready;
-    __syncwarp();
-    MARK(5 + 5 * k);
-    // one warp (rotating, so no warp carries every look-back) publishes the
-    // next group's offsets -- needed one iteration from now
-    if (wib == (k + 1) % W && gn < ngroups) publish(gn, k + 1);
-    MARK(6 + 5 * k);
-    // flush once this group's offsets are published
-    mbar_wait(bar_pub + 8 * par, (k >> 1) & 1);
-    MARK(7 + 5 * k);
-    const unsigned long long P = *(volatile unsigned long long*)&s_Pw[par][wib];
-    if (have && fits) {
-      if (aligned) flush_aligned_stg(a.out, a.nsym, P, cur.C, stg_s);
-      else flush_compact(a.out, a.nsym, P, cur.C, stg_s);
-    } else if (have) {
-      // reference rounds (staging.py:123-146) with capacity cap - 8
-      const bool active = lane < cur.nsl;
-      const uint32_t capw = a.cap - 8;
-      const uint32_t endl = cur.o + cur.c;
-      uint32_t si = 0;
-      while (si < cur.C) {
-        const uint32_t window = si + capw;
-        const unsigned mj = __ballot_sync(0xffffffffu, active && endl > si);
-        const uint32_t jl = __ffs(mj) - 1;
-        const unsigned mk = __ballot_sync(0xffffffffu, active && lane >= jl && endl > window);
-        const uint32_t kl = mk ? __ffs(mk) - 1 : cur.nsl;
-        if (kl == jl) {
-          if (lane == jl) {
-            SR r;
-            r.init(base_s, cur.e);
-            if (!fdecode_global(r, cur.c, a.out, P + cur.o, a.nsym, T)) bad = true;
-          }
-          si = __shfl_sync(0xffffffffu, endl, jl);
-          continue;
-        }
-        const uint32_t temp_end = kl < cur.nsl ? __shfl_sync(0xffffffffu, cur.o, kl & 31) : cur.C;
-        const uint64_t g0w = P + si;
-        const uint64_t gbase = g0w & ~7ull;
-        const bool mine = lane >= jl && lane < kl && cur.c;
-        const uint32_t d = stg_s + 2 * (uint32_t)(P + cur.o - gbase);
-        if (mine) {
-          SR r;
-          r.init(base_s, cur.e);
-          if (!fdecode(r, cur.c, d, T)) bad = true;
-        }
-        __syncwarp();
-        flush_aligned(a.out, a.nsym, g0w, temp_end - si, stg);
-        __syncwarp();
-        si = temp_end;
-      }
-    }
-    __syncwarp();
-    MARK(8 + 5 * k);
-    cur = nxt;
-    wb_cur = wb_next;
-    wb_next = wb_nn;
-    const uint32_t bt = bcur;
-    bcur = bnext;
-    bnext = bnn;
-    bnn = bt;
-  }
-  cp_wait<0>();
-  if (__any_sync(0xffffffffu, bad) && lane == 0) tag_status(a.rep, ep, BH_INVALID);
-  MARK(TRACE_SLOTS - 2);
-  fused_finish(a, ep);
-  MARK(TRACE_SLOTS - 1);
-#undef MARK
-}
 
 
 // ---------------------------------------------------------------------------
@@ -1028,6 +745,8 @@ __device__ unsigned long long lookback_wide(unsigned long long* desc, uint64_t c
   return excl;
 }
 
+constexpr uint32_t MAX_SMEM_TILES = 512;
+
 template <int VAR, int TR>
 __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a) {
 #define MARK(slot)                                                                                  \
@@ -1043,6 +762,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   __shared__ unsigned long long s_ctaoff;
   __shared__ uint32_t s_wsum[32];
   __shared__ uint32_t s_carry;
+  __shared__ uint32_t s_tcnt[MAX_SMEM_TILES];  // symbols per tile of the range (short ranges)
   const uint32_t ep = *(volatile const unsigned int*)a.ws_hdr + 1u;
   const TableHdr* hdr = static_cast<const TableHdr*>(a.table);
   if (VAR == BH_VARIANT_SYNC && !hdr->complete) {
@@ -1059,6 +779,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   const uint32_t W = a.warps;
   const uint64_t G = gridDim.x, cta = blockIdx.x;
   const uint64_t t0 = a.nseq * cta / G, t1 = a.nseq * (cta + 1) / G;
+  const uint32_t nt = (uint32_t)(t1 - t0);
   bool bad = false;
 
   const uint32_t sm_s = smem_u32(sm);
@@ -1073,8 +794,10 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     mbar_expect_tx(bar_ct, 528 + 2 * FB_SIZE);
     bulk_g2s(sm_s + T_C12, tb_ + L.clut12, 2 * FB_SIZE, bar_ct);
     bulk_g2s(sm_s + T_LIM, tb_ + L.lim, 528, bar_ct);  // lim, base (contiguous)
+    // decode tables: wlut8 packed into its own region (spread into the
+    // replicated layout at the end of phase 1), lut12 when present
     mbar_expect_tx(bar_dt, 4096 + (a.has_l12 ? 4 * FB_SIZE : 0));
-    bulk_g2s(sm_s + T_WL, tb_ + L.wlut8, 4096, bar_dt);  // entries packed, spread below
+    bulk_g2s(sm_s + T_WP, tb_ + L.wlut8, 4096, bar_dt);
     if (a.has_l12) bulk_g2s(sm_s + T_L12, tb_ + L.lut12, 4 * FB_SIZE, bar_dt);
   }
   uint64_t tile = t0 + wib;
@@ -1113,53 +836,57 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     const uint32_t de = e - b;
     if (de > 0xffffu || incl > 0xffffu) bad = true;
     a.lane_info[tile * 32 + lane] = (de & 0xffffu) | ((incl - c) << 16);
-    if (lane == 31) a.tile_cnt[tile] = incl;
+    if (lane == 31) {
+      if (nt <= MAX_SMEM_TILES) s_tcnt[tile - t0] = incl;
+      else a.tile_cnt[tile] = incl;
+    }
     wb_a = wb_b;
     buf ^= 1;
   }
   MARK(2);
 
-  // ---- CTA scan of the tile totals, decode tables spread -----------------
+  // ---- tile offsets within the range, CTA aggregate -----------------------
+  // wlut8 replicated 8 ways ([entry][replica] uint4) from its packed copy
   mbar_wait(bar_dt, 0);
-  // spread wlut8 into its 8 replicas ([entry][replica] uint4), highest entries
-  // first: entry e's replicas overwrite packed entries >= e only.  The
-  // barriers also make the range's tile totals visible to the scan below.
-  for (int hi = 255; hi >= 0; hi -= (int)blockDim.x) {
-    const int e = hi - (int)threadIdx.x;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (e >= 0) v = lds128(sm_s + T_WL + 16 * e);
-    __syncthreads();
-    if (e >= 0)
-      for (uint32_t r = 0; r < 8; ++r) sts128(sm_s + T_WL + 128 * e + 16 * r, v);
-    __syncthreads();
-  }
-  const uint32_t nt = (uint32_t)(t1 - t0);
-  const uint32_t nw = blockDim.x >> 5;
+  for (uint32_t i = threadIdx.x; i < 256 * 8; i += blockDim.x)
+    sts128(sm_s + T_WL + 16 * i, lds128(sm_s + T_WP + 16 * (i >> 3)));
+  __syncthreads();  // tile totals and the replicated decode table visible
   uint32_t carry = 0;
-  for (uint32_t base = 0; base < nt; base += blockDim.x) {
-    const uint32_t i = base + threadIdx.x;
-    const uint32_t v = i < nt ? a.tile_cnt[t0 + i] : 0u;
-    uint32_t incl = v;
-    for (int off = 1; off < 32; off <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
-      if ((int)lane >= off) incl += y;
-    }
-    if (lane == 31) s_wsum[wib] = incl;
-    __syncthreads();
+  if (nt <= MAX_SMEM_TILES) {
+    // each warp sums the totals before its tiles itself (phase 2); warp 0 the aggregate
     if (wib == 0) {
-      const uint32_t ws = lane < nw ? s_wsum[lane] : 0u;
-      uint32_t wi = ws;
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, wi, off);
-        if ((int)lane >= off) wi += y;
-      }
-      if (lane < nw) s_wsum[lane] = wi - ws;
-      if (lane == 31) s_carry = wi;
+      uint32_t v = 0;
+      for (uint32_t i = lane; i < nt; i += 32) v += s_tcnt[i];
+      carry = warp_sum(v);
     }
-    __syncthreads();
-    if (i < nt) a.tile_off[t0 + i] = carry + s_wsum[wib] + incl - v;
-    carry += s_carry;
-    __syncthreads();
+  } else {
+    // long ranges: block-wide scan of the totals in the workspace
+    const uint32_t nw = blockDim.x >> 5;
+    for (uint32_t base = 0; base < nt; base += blockDim.x) {
+      const uint32_t i = base + threadIdx.x;
+      const uint32_t v = i < nt ? a.tile_cnt[t0 + i] : 0u;
+      uint32_t incl = v;
+      for (int off = 1; off < 32; off <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+        if ((int)lane >= off) incl += y;
+      }
+      if (lane == 31) s_wsum[wib] = incl;
+      __syncthreads();
+      if (wib == 0) {
+        const uint32_t ws = lane < nw ? s_wsum[lane] : 0u;
+        uint32_t wi = ws;
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, wi, off);
+          if ((int)lane >= off) wi += y;
+        }
+        if (lane < nw) s_wsum[lane] = wi - ws;
+        if (lane == 31) s_carry = wi;
+      }
+      __syncthreads();
+      if (i < nt) a.tile_off[t0 + i] = carry + s_wsum[wib] + incl - v;
+      carry += s_carry;
+      __syncthreads();
+    }
   }
   // warp 0 publishes the CTA aggregate and looks back; the others start decoding
   if (wib == 0) {
@@ -1194,8 +921,17 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     if (tn < t1) wb_b = stage_words(a, tn, wbase + (buf ^ 1) * a.wpb);
     cp_commit();
     const uint32_t info = a.lane_info[tile * 32 + lane];
-    const uint32_t C = a.tile_cnt[tile];
-    const uint32_t toff = a.tile_off[tile];
+    uint32_t C, toff;
+    if (nt <= MAX_SMEM_TILES) {
+      const uint32_t ti = (uint32_t)(tile - t0);
+      uint32_t v = 0;
+      for (uint32_t i = lane; i < ti; i += 32) v += s_tcnt[i];
+      toff = warp_sum(v);
+      C = s_tcnt[ti];
+    } else {
+      C = a.tile_cnt[tile];
+      toff = a.tile_off[tile];
+    }
     cp_wait<1>();
     __syncwarp();
     const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
@@ -1217,6 +953,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       if (!fdecode(r, c, stg_s + 2 * (sh + o), T)) bad = true;
     }
     __syncwarp();
+
     const bool aligned = have_off;
     if (!have_off) {
       mbar_wait(bar_off, 0);
@@ -1225,8 +962,10 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     }
     const unsigned long long P = Pc + toff;
     if (fits) {
+#ifndef BH_X_NOFLUSH
       if (aligned) flush_aligned_stg(a.out, a.nsym, P, C, stg_s);
       else flush_compact(a.out, a.nsym, P, C, stg_s);
+#endif
     } else {
       // reference rounds (staging.py:123-146) with capacity cap - 8
       const bool active = lane < nsl;
@@ -1253,12 +992,13 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         const uint64_t gbase = g0w & ~7ull;
         const bool mine = lane >= jl && lane < kl && c;
         const uint32_t d = stg_s + 2 * (uint32_t)(P + o - gbase);
-        if (mine) {
+            if (mine) {
           SR r;
           r.init(base_s, e);
           if (!fdecode(r, c, d, T)) bad = true;
         }
         __syncwarp();
+
         flush_aligned(a.out, a.nsym, g0w, temp_end - si, stg);
         __syncwarp();
         si = temp_end;
@@ -1294,7 +1034,7 @@ int env_int(const char* name, int dflt) {
 }
 
 struct FusedCfg {
-  uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12, two_phase;
+  uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12;
 };
 
 FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
@@ -1314,10 +1054,9 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   if (cap < 64) cap = 64;
   c.cap = (cap + 7) & ~7u;
   c.has_l12 = !(tune && tune->max_len && tune->max_len <= 8);
-  c.two_phase = env_int("BH_FUSED_V", 2) != 1;
   c.tables = (uint32_t)align16(c.has_l12 ? T_END : T_END_NOL12);
-  // word buffers (two for the two-phase kernel, three for the group pipeline), staging
-  c.per_warp = (uint32_t)align16((c.two_phase ? 8 : 12) * (size_t)c.wpb + 2 * (size_t)c.cap + 32);
+  // two word buffers, staging
+  c.per_warp = (uint32_t)align16(8 * (size_t)c.wpb + 2 * (size_t)c.cap + 32);
   int w = env_int("BH_FUSED_WARPS", 0);
   if (w <= 0) {
     w = (int)((220 * 1024 - c.tables) / c.per_warp);
@@ -1423,13 +1162,9 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   }
   a.trace = g_trace;
-  const void* fn;
-  if (cfg.two_phase)
-    fn = variant == BH_VARIANT_GAP ? (g_trace ? (const void*)k_fused2<BH_VARIANT_GAP, 1> : (const void*)k_fused2<BH_VARIANT_GAP, 0>)
-                                   : (g_trace ? (const void*)k_fused2<BH_VARIANT_SYNC, 1> : (const void*)k_fused2<BH_VARIANT_SYNC, 0>);
-  else
-    fn = variant == BH_VARIANT_GAP ? (g_trace ? (const void*)k_fused<BH_VARIANT_GAP, 1> : (const void*)k_fused<BH_VARIANT_GAP, 0>)
-                                   : (g_trace ? (const void*)k_fused<BH_VARIANT_SYNC, 1> : (const void*)k_fused<BH_VARIANT_SYNC, 0>);
+  const void* fn =
+      variant == BH_VARIANT_GAP ? (g_trace ? (const void*)k_fused2<BH_VARIANT_GAP, 1> : (const void*)k_fused2<BH_VARIANT_GAP, 0>)
+                                : (g_trace ? (const void*)k_fused2<BH_VARIANT_SYNC, 1> : (const void*)k_fused2<BH_VARIANT_SYNC, 0>);
   // launch attributes and occupancy cached per (kernel, threads, smem)
   static std::mutex mu;
   static std::map<std::tuple<const void*, uint32_t, uint32_t>, int> occ;
