@@ -75,6 +75,8 @@ struct FusedArgs {
   uint32_t* lane_info;   // two-phase kernel: per subsequence (entry - boundary) | lane prefix << 16
   uint32_t* tile_cnt;    // two-phase kernel: symbols per tile
   uint32_t* tile_off;    // two-phase kernel: exclusive tile offset within its CTA's range
+  uint16_t* cand;        // SYNC: first-slot count per candidate seed offset (32 per tile)
+  int32_t* tile_dlt;     // SYNC: first-slot count change from the seam fix-up
   DevReport* rep;
   unsigned int* ws_hdr;  // [0] epoch of the last completed call, [1] CTAs done
   uint32_t wpb;          // words per tile buffer (multiple of 4)
@@ -559,10 +561,15 @@ __device__ __forceinline__ void gap_window(const FusedArgs& a, uint64_t tile, ui
 // to the tile buffer's first bit `wb0`.  GAP: boundary + gap byte; SYNC:
 // intra-sequence chain rounds plus the seam seed from the predecessor tile's
 // published final exit.
+// SYNC modes: seed_o < 0 -- speculative (lane 0 entered at its boundary); the
+// counts of the first slot for all 32 candidate seeds go to cand_c, and the
+// tile publishes its exit when no candidate changes it (else a DEP marker);
+// seed_o >= 0 -- the true seed offset is known: the final state is computed
+// and the exit published.
 template <int VAR>
 __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, uint64_t tile, uint32_t base_s,
                                             uint64_t wb0, uint32_t nsl, uint32_t ep, uint32_t& e, uint32_t& c,
-                                            bool& bad) {
+                                            bool& bad, int32_t seed_o = -1, uint32_t* cand_out = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t sb = a.sb;
   const uint64_t j0 = tile * a.sps;
@@ -621,14 +628,16 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
       indep = __all_sync(0xffffffffu, cand_x == x0);
     }
     const uint32_t xlast = __shfl_sync(0xffffffffu, x, nsl - 1);
-    if (lane == 0 && indep) st_release(a.exit_desc + tile, mkdesc(ep, D_INC, wb0 + xlast));
-    if (tile > 0) {
-      unsigned long long d = 0;
-      if (lane == 0) {
-        while (!desc_ready(d = ld_acquire(a.exit_desc + tile - 1), ep)) __nanosleep(20);
-      }
-      const uint64_t seed = __shfl_sync(0xffffffffu, (unsigned long long)(d & D_VAL), 0);
-      const uint32_t o = (uint32_t)(seed - wb0) - b0;
+    if (seed_o < 0) {
+      // speculative: publish the exit when it does not depend on the seed
+      if (cand_out) *cand_out = cand_c;
+      if (lane == 0) st_release(a.exit_desc + tile, mkdesc(ep, indep ? D_INC : D_AGG, indep ? wb0 + xlast : 0));
+#ifdef BH_X_DEPSTAT
+      if (lane == 0 && !indep) atomicAdd(&a.rep->pad[3], 1ull);
+      if (lane == 0 && tile > 0) atomicAdd(&a.rep->pad[3], 1ull << 32);
+#endif
+    } else if (tile > 0) {
+      const uint32_t o = (uint32_t)seed_o;
       const uint32_t sc = __shfl_sync(0xffffffffu, cand_c, o & 31);
       const uint32_t sx = __shfl_sync(0xffffffffu, cand_x, o & 31);
       if (o >= 32) bad = true;
@@ -652,10 +661,8 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
           dprev2 = dnow;
         }
       }
-      if (!indep) {
-        const uint32_t xl = __shfl_sync(0xffffffffu, x, nsl - 1);
-        if (lane == 0) st_release(a.exit_desc + tile, mkdesc(ep, D_INC, wb0 + xl));
-      }
+      const uint32_t xl = __shfl_sync(0xffffffffu, x, nsl - 1);
+      if (lane == 0) st_release(a.exit_desc + tile, mkdesc(ep, D_INC, wb0 + xl));
     }
   }
   if (!active) c = 0;
@@ -825,8 +832,9 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     cp_wait<1>();
     __syncwarp();
     const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
-    uint32_t e, c;
-    tile_counts<VAR>(a, T, tile, wbase_s + 4 * a.wpb * buf, wb_a, nsl, ep, e, c, bad);
+    uint32_t e, c, cand = 0;
+    tile_counts<VAR>(a, T, tile, wbase_s + 4 * a.wpb * buf, wb_a, nsl, ep, e, c, bad, -1, &cand);
+    if (VAR == BH_VARIANT_SYNC) a.cand[tile * 32 + lane] = (uint16_t)min(cand, 0xffffu);
     uint32_t incl = c;
     for (int off = 1; off < 32; off <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
@@ -842,6 +850,94 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     }
     wb_a = wb_b;
     buf ^= 1;
+  }
+  cp_wait<0>();
+  if (VAR == BH_VARIANT_SYNC) {
+    // Seam fix-up (inter_sync, sync_decoder.py:116-149).  Every exit that does
+    // not depend on the seed was published during the count loop, so the
+    // true seed of most tiles is known now: lane j of the warp takes the
+    // warp's tile j of a 32-tile chunk, reads the predecessor's exit and swaps
+    // in the first slot's count for that seed (the other slots are unchanged
+    // because every candidate seed leads to the same first exit).  Tiles whose
+    // exit depends on the seed (or whose predecessor's does) are finished one
+    // at a time in tile order: the words are staged again and the tile is
+    // re-synchronised from the known seed.
+    for (uint64_t kb = 0;; kb += 32) {
+      const uint64_t tk = t0 + wib + (kb + lane) * W;
+      const bool mine = tk < t1;
+      if (!__any_sync(0xffffffffu, mine)) break;
+      bool serial = false;
+      if (mine && tk > 0) {
+        unsigned long long dp, ds = ld_acquire(a.exit_desc + tk);
+        while (!desc_ready(dp = ld_acquire(a.exit_desc + tk - 1), ep)) __nanosleep(32);
+        if ((ds & D_INC) && (dp & D_INC)) {
+          const uint32_t o = (uint32_t)((dp & D_VAL) - tk * a.seq_bits);
+          if (o >= 32) {
+            bad = true;
+          } else if (o) {
+            const int32_t dl = (int32_t)a.cand[tk * 32 + o] - (int32_t)a.cand[tk * 32];
+            a.tile_dlt[tk] = dl;
+            a.lane_info[tk * 32] = o;  // first slot enters at the seed; prefix 0
+            if (nt <= MAX_SMEM_TILES) s_tcnt[tk - t0] += (uint32_t)dl;
+            else a.tile_cnt[tk] += (uint32_t)dl;
+          } else {
+            a.tile_dlt[tk] = 0;
+          }
+        } else {
+          serial = true;
+        }
+      } else if (mine) {
+        a.tile_dlt[tk] = 0;
+      }
+      unsigned sm_mask = __ballot_sync(0xffffffffu, serial);
+      while (sm_mask) {
+        const uint32_t j = __ffs(sm_mask) - 1;
+        sm_mask &= sm_mask - 1;
+        const uint64_t st = t0 + wib + (kb + j) * W;
+        unsigned long long dp = 0;
+        if (lane == 0)
+          while (!((dp = ld_acquire(a.exit_desc + st - 1)) & D_INC) || !desc_ready(dp, ep)) __nanosleep(32);
+        dp = __shfl_sync(0xffffffffu, dp, 0);
+        const uint32_t o = (uint32_t)((dp & D_VAL) - st * a.seq_bits);
+        const unsigned long long ds = ld_acquire(a.exit_desc + st);
+        if (ds & D_INC) {  // seed-independent tile behind a dependent one
+          if (o >= 32) {
+            bad = true;
+          } else if (lane == 0) {
+            const int32_t dl = (int32_t)a.cand[st * 32 + o] - (int32_t)a.cand[st * 32];
+            a.tile_dlt[st] = dl;
+            a.lane_info[st * 32] = o;
+            if (nt <= MAX_SMEM_TILES) s_tcnt[st - t0] += (uint32_t)dl;
+            else a.tile_cnt[st] += (uint32_t)dl;
+          }
+          __syncwarp();
+          continue;
+        }
+        // dependent tile: stage its words again and synchronise from the seed
+        const uint64_t wbs = stage_words(a, st, wbase);
+        cp_commit();
+        cp_wait<0>();
+        __syncwarp();
+        const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - st * a.sps);
+        uint32_t e, c;
+        tile_counts<VAR>(a, T, st, wbase_s, wbs, nsl, ep, e, c, bad, (int32_t)min(o, 255u));
+        uint32_t incl = c;
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+          if ((int)lane >= off) incl += y;
+        }
+        const uint32_t b = (uint32_t)((st * a.sps + lane) * a.sb - wbs);
+        const uint32_t de = e - b;
+        if (de > 0xffffu || incl > 0xffffu) bad = true;
+        a.lane_info[st * 32 + lane] = (de & 0xffffu) | ((incl - c) << 16);
+        if (lane == 31) {
+          a.tile_dlt[st] = 0;
+          if (nt <= MAX_SMEM_TILES) s_tcnt[st - t0] = incl;
+          else a.tile_cnt[st] = incl;
+        }
+        __syncwarp();
+      }
+    }
   }
   MARK(2);
 
@@ -938,7 +1034,8 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     const uint32_t base_s = wbase_s + 4 * a.wpb * buf;
     const uint32_t b = (uint32_t)((tile * a.sps + lane) * a.sb - wb_a);
     const uint32_t e = b + (info & 0xffffu);
-    const uint32_t o = info >> 16;
+    uint32_t o = info >> 16;
+    if (VAR == BH_VARIANT_SYNC && lane > 0) o += (uint32_t)a.tile_dlt[tile];  // seam fix of slot 0
     const uint32_t on = __shfl_down_sync(0xffffffffu, o, 1);
     const uint32_t c = lane < nsl ? (lane == 31 ? C : on) - o : 0u;
     if (!have_off) {
@@ -1113,8 +1210,9 @@ extern "C" int bh_fused_supported(const bh_stream* s, int variant) {
 
 // workspace: [64 B header: epoch, CTA-done counter][cnt desc][exit desc]
 //            [lane info u32 x 32 per tile][tile count u32][tile offset u32]
+//            [seed candidates u16 x 32 per tile][first-slot delta i32]
 extern "C" size_t bh_fused_workspace_bytes(const bh_stream* s, int, const bh_tune*) {
-  return 64 + 16 * nseq_of(s) + 4 * 34 * nseq_of(s) + 256;
+  return 64 + 16 * nseq_of(s) + 4 * 34 * nseq_of(s) + 64 * nseq_of(s) + 4 * nseq_of(s) + 256;
 }
 
 extern "C" int bh_workspace_reset(void* ws, size_t bytes, void* cuda_stream) {
@@ -1148,6 +1246,8 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.lane_info = reinterpret_cast<uint32_t*>(a.exit_desc + nseq);
   a.tile_cnt = a.lane_info + 32 * nseq;
   a.tile_off = a.tile_cnt + nseq;
+  a.cand = reinterpret_cast<uint16_t*>(a.tile_off + nseq);
+  a.tile_dlt = reinterpret_cast<int32_t*>(a.cand + 32 * nseq);
   a.rep = static_cast<DevReport*>(report_dev);
   a.wpb = cfg.wpb;
   a.cap = cfg.cap;
