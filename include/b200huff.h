@@ -51,6 +51,10 @@ typedef struct bh_stream {
     uint32_t max_codes;          /* capacity the table blob was sized for */
     const uint8_t *gap_dev;      /* num_subseqs forward skips, or NULL */
     const void *table_dev;       /* blob from bh_table_build*() */
+    uint32_t first_entry;        /* bit offset of the first codeword start; 0 for a whole
+                                    stream, the chunk's first gap byte for a sequence-aligned
+                                    chunk of a longer stream (sharded decode; fused path only) */
+    uint32_t reserved;
 } bh_stream;
 
 /* Tuning knobs (tuner.py:29-40 TunerConfig, staging.py:28 DEFAULT_CAPACITY). */

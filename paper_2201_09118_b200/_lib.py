@@ -32,6 +32,7 @@ class Stream(C.Structure):
         ("words_dev", P), ("total_bits", U64), ("symbol_count", U64),
         ("subseq_bits", U32), ("subseqs_per_seq", U32), ("symbol_width", U32),
         ("max_codes", U32), ("gap_dev", P), ("table_dev", P),
+        ("first_entry", U32), ("reserved", U32),
     ]
 
 

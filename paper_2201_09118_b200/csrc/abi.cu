@@ -282,6 +282,7 @@ extern "C" int bh_decode_async(const bh_stream* s, int variant, const bh_tune* t
   if (variant == BH_VARIANT_GAP && !s->gap_dev && s->total_bits) return BH_NOTPRESENT;
   if (s->total_bits && use_fused(s, variant, tune))
     return bh_fused_decode(s, variant, tune, out_dev, ws, ws_bytes, report_dev, cuda_stream);
+  if (s->first_entry) return BH_BAD_ARGUMENT;  // chunked streams: fused path only
   int rc = bh_report_init(report_dev, cuda_stream);
   if (rc) return rc;
   if (s->total_bits == 0) {

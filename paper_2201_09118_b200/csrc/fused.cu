@@ -85,6 +85,7 @@ struct FusedArgs {
   uint32_t per_warp_bytes;
   uint32_t tables_bytes;
   uint32_t has_l12;      // 12-bit second-level table staged (codes longer than 8 bits)
+  uint32_t first_entry;  // bh_stream.first_entry
   unsigned long long* trace;  // debug timeline (TR instantiation only)
 };
 
@@ -595,6 +596,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
     }
   } else {
     stop = min(b + sb, tbr);
+    if (tile == 0 && lane == 0) e = x = b + a.first_entry;  // chunk of a longer stream
     if (active && e < stop) {
       SR r;
       r.init(base_s, e);
@@ -1255,6 +1257,7 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.per_warp_bytes = cfg.per_warp;
   a.tables_bytes = cfg.tables;
   a.has_l12 = cfg.has_l12;
+  a.first_entry = s->first_entry;
   static int sms = 0;
   if (!sms) {
     int dev = 0;

@@ -16,6 +16,9 @@ Timing over ranks is the max of the per-rank device times (``max_over_ranks``).
 from __future__ import annotations
 
 import heapq
+from dataclasses import dataclass
+
+import numpy as np
 
 
 def lpt_assign(sizes, world: int) -> list[list[int]]:
@@ -72,3 +75,56 @@ def max_over_ranks(value: float, group=None) -> float:
     t = torch.tensor([float(value)], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     return float(t.item())
+
+
+@dataclass(frozen=True)
+class Chunk:
+    """A sequence-aligned piece of one stream, decodable on its own.
+
+    ``word0`` is its first 32-bit payload word, ``total_bits`` its bit span
+    (it ends at the next chunk's first codeword start, so codewords belong to
+    the chunk they start in, exactly like gap windows), ``sub0``/``nsub`` its
+    slice of the gap array, ``first_entry`` the bit offset of its first
+    codeword (the first gap byte; 0 for the stream's first chunk), ``n`` the
+    symbols it decodes and ``out0`` where they go in the stream's output.
+    """
+
+    q0: int
+    q1: int
+    word0: int
+    total_bits: int
+    sub0: int
+    nsub: int
+    first_entry: int
+    n: int
+    out0: int
+
+
+def chunk_stream(total_bits: int, subseq_bits: int, subseqs_per_seq: int, gap, subseq_counts,
+                 nchunks: int) -> list[Chunk]:
+    """Cut a stream into `nchunks` sequence-aligned chunks.
+
+    `gap` is the stream's forward-skip array and `subseq_counts` the symbols
+    per subsequence (the gap count pass), both recorded at encode time; they
+    give every chunk's entry bit and symbol count without decoding.
+    """
+    gap = np.asarray(gap, dtype=np.int64)
+    cnt = np.asarray(subseq_counts, dtype=np.int64)
+    nsub = -(-total_bits // subseq_bits)
+    nseq = -(-nsub // subseqs_per_seq)
+    seq_bits = subseq_bits * subseqs_per_seq
+    if seq_bits % 32:
+        raise ValueError("chunking needs sequences that are a whole number of 32-bit words")
+    oi = np.concatenate([[0], np.cumsum(cnt)])
+    out = []
+    for q0, q1 in sequence_ranges(nseq, max(1, min(nchunks, nseq))):
+        if q0 == q1:
+            continue
+        s0, s1 = q0 * subseqs_per_seq, min(q1 * subseqs_per_seq, nsub)
+        b0 = q0 * seq_bits
+        end = total_bits if s1 >= nsub else min(s1 * subseq_bits + int(gap[s1]), total_bits)
+        tb = end - b0
+        ns = -(-tb // subseq_bits)
+        out.append(Chunk(q0, q1, b0 // 32, tb, s0, ns, int(gap[s0]) if s0 else 0,
+                         int(oi[s1] - oi[s0]), int(oi[s0])))
+    return out

@@ -135,3 +135,28 @@ def test_decode_fails_loudly_without_cuda():
         ph.gap_decoder.decode(st)
     with pytest.raises(RuntimeError, match="CUDA"):
         ph.sync_decoder.decode(st)
+
+
+def test_chunk_stream_partitions_symbols_and_windows():
+    """Sequence-aligned chunks (sharded decode): every symbol in exactly one
+    chunk, chunk spans end at the next chunk's first codeword start."""
+    import numpy as np
+    from paper_2201_09118_b200 import shard
+    rng = np.random.default_rng(3)
+    sb, sps = 128, 4
+    tb = 128 * 4 * 37 + 77
+    nsub = -(-tb // sb)
+    gap = rng.integers(0, 20, nsub).astype(np.uint8)
+    gap[0] = 0
+    counts = rng.integers(0, 60, nsub)
+    for k in (1, 2, 5, 10, 37, 100):
+        ch = shard.chunk_stream(tb, sb, sps, gap, counts, k)
+        assert sum(c.n for c in ch) == counts.sum()
+        assert [c.out0 for c in ch] == list(np.cumsum([0] + [c.n for c in ch])[:-1])
+        assert ch[0].q0 == 0 and ch[-1].q1 == -(-nsub // sps)
+        for a, b in zip(ch, ch[1:]):
+            assert a.q1 == b.q0
+            assert a.word0 * 32 + a.total_bits == b.word0 * 32 + b.first_entry  # ends at the next entry
+            assert b.first_entry == gap[b.sub0]
+        assert ch[-1].word0 * 32 + ch[-1].total_bits == tb
+        assert all(c.sub0 + c.nsub <= nsub for c in ch)
