@@ -45,6 +45,8 @@ struct TableHdr {
 //   clut8 u8[256]    next 8 bits -> (ncode<<3) | (bits-1) over every whole
 //                    codeword inside the 8 bits, 0 if the first one is longer
 //   lut12 u32[4096]  next 12 bits -> sym | len<<16 for codes of <= 12 bits, else 0
+//   wlut12 uint4[4096] next 12 bits -> up to 6 whole codewords, wlut8's format
+//                    (the fused kernels' decode table for long-code books)
 //   clut12 u16[4096] next 12 bits -> starts | bits<<12 over every whole codeword
 //                    inside the 12 bits (count pass): bit i of `starts` is set
 //                    when a codeword starts at offset i, `bits` is where the
@@ -59,7 +61,7 @@ constexpr int FB_SIZE = 1 << FB;
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct TableLayout {
-  size_t lut, cnt, dlut8, clut8, wlut8, lut12, clut12, lim, base, lj, ljsym, ljlen, total;
+  size_t lut, cnt, dlut8, clut8, wlut8, lut12, clut12, wlut12, lim, base, lj, ljsym, ljlen, total;
   __host__ __device__ explicit TableLayout(uint32_t max_codes) {
     lut = TABLE_HDR_BYTES;
     cnt = lut + sizeof(uint32_t) * LUT_SIZE;
@@ -68,7 +70,8 @@ struct TableLayout {
     wlut8 = align16(clut8 + 256);
     lut12 = align16(wlut8 + 16 * 256);
     clut12 = lut12 + 4 * (size_t)FB_SIZE;
-    lim = align16(clut12 + 2 * (size_t)FB_SIZE);
+    wlut12 = align16(clut12 + 2 * (size_t)FB_SIZE);
+    lim = align16(wlut12 + 16 * (size_t)FB_SIZE);
     base = lim + 8 * 33;
     lj = align16(base + 8 * 33);
     ljsym = align16(lj + sizeof(uint32_t) * (size_t)max_codes);

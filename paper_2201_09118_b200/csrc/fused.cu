@@ -86,22 +86,25 @@ struct FusedArgs {
   uint32_t tables_bytes;
   uint32_t has_l12;      // 12-bit second-level table staged (codes longer than 8 bits)
   uint32_t first_entry;  // bh_stream.first_entry
+  uint32_t wide;         // table layout: 1 = wlut12, 0 = replicated wlut8 (+ lut12 if has_l12)
+  uint32_t t_lim, t_c12, t_wp, t_l12;  // shared-memory table offsets (bytes)
   unsigned long long* trace;  // debug timeline (TR instantiation only)
 };
 
 constexpr unsigned long long FUSED_MARK = 0xF05EDull;  // rep->pad[2]: report written by k_fused
 
-// shared-memory table layout inside the CTA (bytes)
-// wlut8 is replicated 8 times ([entry][8] uint4): an LDS.128 is served per
-// quarter-warp, so lane l reading replica l%8 never conflicts (32 KB).
-constexpr uint32_t T_WL = 0;                      // uint4 [256][8] replicated wlut8
-constexpr uint32_t T_LIM = T_WL + 256 * 8 * 16;   // u64 [33]
-constexpr uint32_t T_BASE = T_LIM + 33 * 8;       // i64 [33]
-constexpr uint32_t T_C12 = T_BASE + 33 * 8;       // u16 [4096] 12-bit count table
-constexpr uint32_t T_WP = T_C12 + 2 * FB_SIZE;    // uint4 [256] packed wlut8 (bulk-copy target)
-constexpr uint32_t T_L12 = T_WP + 4096;           // u32 [4096] second level: codes of 9..12 bits (optional)
-constexpr uint32_t T_END_NOL12 = T_L12;
-constexpr uint32_t T_END = T_L12 + 4 * FB_SIZE;
+// Shared-memory table layouts inside the CTA (byte offsets, FusedArgs.t_*):
+//   narrow (short codes): the 8-bit decode table wlut8 replicated 8 times
+//     ([entry][8] uint4, 32 KB: an LDS.128 is served per quarter-warp, so
+//     lane l reading replica l%8 never conflicts), lim, base, the 12-bit count
+//     table, the packed wlut8 bulk-copy target (4 KB) and, for codes longer
+//     than 8 bits, the 12-bit single-codeword table lut12 (16 KB);
+//   wide (long codes, more than ~1.5 bits per symbol): the 12-bit decode
+//     table wlut12 (64 KB, one lookup covers twice the bits), lim, base and
+//     the count table.
+constexpr uint32_t T_LIMBASE = 2 * 33 * 8;  // lim u64[33], base i64[33] (contiguous)
+constexpr uint32_t T_NARROW_DEC = 256 * 8 * 16;
+constexpr uint32_t T_WIDE_DEC = 16 * FB_SIZE;
 
 __device__ __forceinline__ void tag_status(DevReport* rep, uint32_t ep, uint32_t status) {
   unsigned long long v = ((unsigned long long)ep << 32) | (unsigned long long)(0x7fffffffu - status);
@@ -187,7 +190,9 @@ struct SR {
 };
 
 struct FTab {
-  uint32_t wl;     // this lane's column of the replicated wlut8 (shared address)
+  uint32_t wl;     // decode table: this lane's replica of wlut8, or wlut12 (shared address)
+  uint32_t dsh;    // window shift of the decode index: 24 (8-bit) or 20 (12-bit)
+  uint32_t dst;    // entry stride shift: 7 (8 replicas x 16 B) or 4 (16 B)
   uint32_t l12;    // shared address of lut12
   uint32_t c12;    // shared address of clut12
   uint32_t lim;    // shared address of lim (u64[33])
@@ -223,13 +228,13 @@ __device__ __forceinline__ uint32_t flong(uint32_t win, const FTab& T) {
 
 // one codeword: sym | len<<16 (0 = no codeword matches)
 __device__ __forceinline__ uint32_t fone(uint32_t win, const FTab& T) {
-  const uint4 w = lds128(T.wl + ((win >> 24) << 7));
+  const uint4 w = lds128(T.wl + ((win >> T.dsh) << T.dst));
   if (w.w) return (w.x & 0xffffu) | (((w.w >> 16) & 15u) << 16);
   return flong(win, T);
 }
 
 __device__ __forceinline__ uint32_t flen(uint32_t win, const FTab& T) {
-  const uint32_t y = lds128(T.wl + ((win >> 24) << 7)).w;
+  const uint32_t y = lds128(T.wl + ((win >> T.dsh) << T.dst)).w;
   if (y) return (y >> 16) & 15u;
   return (flong(win, T) >> 16) & 0xffu;
 }
@@ -287,12 +292,12 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
 // overwritten by its next stores); the last entries store predicated, so lane
 // ranges stay disjoint even for corrupt (non-contiguous) windows.
 __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const FTab& T) {
-  const uint32_t wl = pin(T.wl);
+  const uint32_t wl = pin(T.wl), dsh = T.dsh, dstr = T.dst;
   int32_t k = (int32_t)c;
 #if !defined(BH_FDEC_PRED)
   while (k >= 7) {
     const uint32_t win = r.peek();
-    const uint4 w = lds128(wl + ((win >> 24) << 7));
+    const uint4 w = lds128(wl + ((win >> dsh) << dstr));
     if (w.w) {
       // one halfword store, then three aligned word stores: an odd start
       // shifts the entry by one halfword (the seventh halfword written is
@@ -323,7 +328,7 @@ __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const F
 #endif
   while (k > 0) {
     const uint32_t win = r.peek();
-    const uint4 w = lds128(wl + ((win >> 24) << 7));
+    const uint4 w = lds128(wl + ((win >> dsh) << dstr));
     if (w.w) {
       const int32_t n = (int32_t)((w.w >> 4) & 15u);
       const int32_t m = n < k ? n : k;
@@ -800,25 +805,32 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     mbar_init(bar_dt, 1);
     mbar_init(bar_off, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(bar_ct, 528 + 2 * FB_SIZE);
-    bulk_g2s(sm_s + T_C12, tb_ + L.clut12, 2 * FB_SIZE, bar_ct);
-    bulk_g2s(sm_s + T_LIM, tb_ + L.lim, 528, bar_ct);  // lim, base (contiguous)
-    // decode tables: wlut8 packed into its own region (spread into the
-    // replicated layout at the end of phase 1), lut12 when present
-    mbar_expect_tx(bar_dt, 4096 + (a.has_l12 ? 4 * FB_SIZE : 0));
-    bulk_g2s(sm_s + T_WP, tb_ + L.wlut8, 4096, bar_dt);
-    if (a.has_l12) bulk_g2s(sm_s + T_L12, tb_ + L.lut12, 4 * FB_SIZE, bar_dt);
+    mbar_expect_tx(bar_ct, T_LIMBASE + 2 * FB_SIZE);
+    bulk_g2s(sm_s + a.t_c12, tb_ + L.clut12, 2 * FB_SIZE, bar_ct);
+    bulk_g2s(sm_s + a.t_lim, tb_ + L.lim, T_LIMBASE, bar_ct);  // lim, base (contiguous)
+    if (a.wide) {
+      mbar_expect_tx(bar_dt, T_WIDE_DEC);
+      bulk_g2s(sm_s, tb_ + L.wlut12, T_WIDE_DEC, bar_dt);
+    } else {
+      // wlut8 packed into its own region (spread into the replicated layout
+      // at the end of phase 1), lut12 when present
+      mbar_expect_tx(bar_dt, 4096 + (a.has_l12 ? 4 * FB_SIZE : 0));
+      bulk_g2s(sm_s + a.t_wp, tb_ + L.wlut8, 4096, bar_dt);
+      if (a.has_l12) bulk_g2s(sm_s + a.t_l12, tb_ + L.lut12, 4 * FB_SIZE, bar_dt);
+    }
   }
   uint64_t tile = t0 + wib;
   uint64_t wb_a = 0, wb_b = 0;
   if (tile < t1) wb_a = stage_words(a, tile, wbase);
   cp_commit();
   FTab T;
-  T.wl = sm_s + T_WL + 16 * (lane & 7);
-  T.lim = sm_s + T_LIM;
-  T.base = sm_s + T_BASE;
-  T.l12 = a.has_l12 ? sm_s + T_L12 : 0u;
-  T.c12 = sm_s + T_C12;
+  T.wl = a.wide ? sm_s : sm_s + 16 * (lane & 7);
+  T.dsh = a.wide ? 32 - FB : 24;
+  T.dst = a.wide ? 4 : 7;
+  T.lim = sm_s + a.t_lim;
+  T.base = sm_s + a.t_lim + 33 * 8;
+  T.l12 = (!a.wide && a.has_l12) ? sm_s + a.t_l12 : 0u;
+  T.c12 = sm_s + a.t_c12;
   T.t = table_view(a.table, a.max_codes, hdr->ncodes);
   T.kind = hdr->kind;
   __syncthreads();  // barriers initialised
@@ -946,8 +958,9 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   // ---- tile offsets within the range, CTA aggregate -----------------------
   // wlut8 replicated 8 ways ([entry][replica] uint4) from its packed copy
   mbar_wait(bar_dt, 0);
-  for (uint32_t i = threadIdx.x; i < 256 * 8; i += blockDim.x)
-    sts128(sm_s + T_WL + 16 * i, lds128(sm_s + T_WP + 16 * (i >> 3)));
+  if (!a.wide)
+    for (uint32_t i = threadIdx.x; i < 256 * 8; i += blockDim.x)
+      sts128(sm_s + 16 * i, lds128(sm_s + a.t_wp + 16 * (i >> 3)));
   __syncthreads();  // tile totals and the replicated decode table visible
   uint32_t carry = 0;
   if (nt <= MAX_SMEM_TILES) {
@@ -1133,7 +1146,7 @@ int env_int(const char* name, int dflt) {
 }
 
 struct FusedCfg {
-  uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12;
+  uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12, wide, t_lim, t_c12, t_wp, t_l12;
 };
 
 FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
@@ -1153,7 +1166,23 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   if (cap < 64) cap = 64;
   c.cap = (cap + 7) & ~7u;
   c.has_l12 = !(tune && tune->max_len && tune->max_len <= 8);
-  c.tables = (uint32_t)align16(c.has_l12 ? T_END : T_END_NOL12);
+  // long codes and more than ~1.5 bits per symbol: the 12-bit decode table
+  // covers twice the bits per lookup (short-code books already get six
+  // symbols out of the conflict-free 8-bit one)
+  c.wide = c.has_l12 && 2 * s->total_bits > 3 * s->symbol_count;
+  if (env_int("BH_FUSED_WIDE", -1) >= 0) c.wide = env_int("BH_FUSED_WIDE", 0) != 0;
+  if (c.wide) {
+    c.t_lim = T_WIDE_DEC;
+    c.t_c12 = c.t_lim + T_LIMBASE;
+    c.t_wp = c.t_l12 = 0;
+    c.tables = (uint32_t)align16(c.t_c12 + 2 * FB_SIZE);
+  } else {
+    c.t_lim = T_NARROW_DEC;
+    c.t_c12 = c.t_lim + T_LIMBASE;
+    c.t_wp = c.t_c12 + 2 * FB_SIZE;
+    c.t_l12 = c.t_wp + 4096;
+    c.tables = (uint32_t)align16(c.t_l12 + (c.has_l12 ? 4 * FB_SIZE : 0));
+  }
   // two word buffers, staging
   c.per_warp = (uint32_t)align16(8 * (size_t)c.wpb + 2 * (size_t)c.cap + 32);
   int w = env_int("BH_FUSED_WARPS", 0);
@@ -1258,6 +1287,11 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.tables_bytes = cfg.tables;
   a.has_l12 = cfg.has_l12;
   a.first_entry = s->first_entry;
+  a.wide = cfg.wide;
+  a.t_lim = cfg.t_lim;
+  a.t_c12 = cfg.t_c12;
+  a.t_wp = cfg.t_wp;
+  a.t_l12 = cfg.t_l12;
   static int sms = 0;
   if (!sms) {
     int dev = 0;

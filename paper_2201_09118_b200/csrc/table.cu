@@ -206,14 +206,35 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
   uint8_t* clut8 = reinterpret_cast<uint8_t*>(reinterpret_cast<char*>(blob) + L.clut8);
   uint32_t* lut12 = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(blob) + L.lut12);
   uint16_t* clut12 = reinterpret_cast<uint16_t*>(reinterpret_cast<char*>(blob) + L.clut12);
-  __syncthreads();  // s_lut is reused for the 12-bit codes below
-  uint16_t* s_len12 = reinterpret_cast<uint16_t*>(s_lut);  // 4096 lengths (8 KB)
+  __shared__ uint32_t s_l12[FB_SIZE];  // sym | len<<16 of codes <= 12 bits (16 KB)
   for (int v = threadIdx.x; v < FB_SIZE; v += blockDim.x) {
     uint32_t e = slow_lookup(t, (uint32_t)v << (32 - FB));
     const uint32_t len = (e >> 16) & 0xff;
     lut12[v] = len <= (uint32_t)FB ? e : 0u;
-    s_len12[v] = (uint16_t)(len <= (uint32_t)FB ? len : 0u);
+    s_l12[v] = len <= (uint32_t)FB ? e : 0u;
   }
+  __syncthreads();
+  // up to six whole codewords of the 12-bit window (wide decode table)
+  uint4* wlut12 = reinterpret_cast<uint4*>(reinterpret_cast<char*>(blob) + L.wlut12);
+  for (int v = threadIdx.x; v < FB_SIZE; v += blockDim.x) {
+    uint32_t p6 = 0, n6 = 0, sy[6] = {0, 0, 0, 0, 0, 0}, l0 = 0;
+    while (n6 < 6 && p6 < (uint32_t)FB) {
+      const uint32_t f = s_l12[((uint32_t)v << p6) & (FB_SIZE - 1)];
+      const uint32_t len = (f >> 16) & 0xff;
+      if (len == 0 || p6 + len > (uint32_t)FB) break;
+      if (n6 == 0) l0 = len;
+      sy[n6++] = f & 0xffff;
+      p6 += len;
+    }
+    uint4 wl;
+    wl.x = sy[0] | (sy[1] << 16);
+    wl.y = sy[2] | (sy[3] << 16);
+    wl.z = sy[4] | (sy[5] << 16);
+    wl.w = n6 ? (p6 | (n6 << 4) | (l0 << 16)) : 0u;
+    wlut12[v] = wl;
+  }
+  uint16_t* s_len12 = reinterpret_cast<uint16_t*>(s_lut);  // 4096 lengths (8 KB)
+  for (int v = threadIdx.x; v < FB_SIZE; v += blockDim.x) s_len12[v] = (uint16_t)((s_l12[v] >> 16) & 0xff);
   __syncthreads();
   // count table: every whole codeword of the 12-bit window (zero fill past the
   // window cannot change a match of a codeword that lies inside it)
