@@ -527,6 +527,40 @@ __device__ __forceinline__ void flush_aligned_stg(uint16_t* __restrict__ out, ui
   }
 }
 
+// Same as flush_aligned_stg, but the whole 16-byte chunks leave shared memory
+// as ONE bulk (TMA) copy issued by lane 0 -- no registers or load/store
+// instructions per chunk.  The staging must not be rewritten before the copy
+// has read it (bulk_read_wait).  Returns whether a copy was issued.
+__device__ __forceinline__ bool flush_bulk(uint16_t* __restrict__ out, uint64_t nsym, uint64_t P, uint32_t C,
+                                           uint32_t stg_s) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint64_t a0 = P & ~7ull, g1 = P + C;
+  const uint64_t f0 = (P + 7) & ~7ull;
+  const uint64_t f1 = (g1 < nsym ? g1 : nsym) & ~7ull;
+  const bool bulk = f1 > f0;
+  if (bulk && lane == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging stores -> async proxy
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                 ::"l"(out + f0), "r"(stg_s + 2 * (uint32_t)(f0 - a0)), "r"((uint32_t)(2 * (f1 - f0)))
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  }
+  const uint64_t hend = f0 < g1 ? f0 : g1;
+  const uint64_t tbeg = f1 > hend ? f1 : hend;
+  const uint32_t nh = (uint32_t)(hend - P), nt = (uint32_t)(g1 - tbeg);
+  if (lane < nh) {
+    const uint64_t g = P + lane;
+    if (g < nsym) out[g] = (uint16_t)lds16(stg_s + 2 * (uint32_t)(g - a0));
+  } else if (lane >= 8 && lane - 8 < nt) {
+    const uint64_t g = tbeg + (lane - 8);
+    if (g < nsym) out[g] = (uint16_t)lds16(stg_s + 2 * (uint32_t)(g - a0));
+  }
+  return bulk;
+}
+__device__ __forceinline__ void bulk_read_wait() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+
 // 128-bit flush of [g0, g0+len) from staging aligned to g0 (stg[0] <-> g0 & ~7)
 __device__ __forceinline__ void flush_aligned(uint16_t* __restrict__ out, uint64_t nsym, uint64_t g0, uint32_t len,
                                               const uint16_t* stg) {
@@ -1025,7 +1059,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   buf = 0;
   if (tile < t1) wb_a = stage_words(a, tile, wbase);
   cp_commit();
-  bool have_off = false;
+  bool have_off = false, bulk_pending = false;
   unsigned long long Pc = 0;
   for (; tile < t1; tile += W) {
     const uint64_t tn = tile + W;
@@ -1059,6 +1093,11 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     }
     const bool fits = C + 16 <= a.cap;
     const uint32_t sh = have_off ? (uint32_t)(Pc + toff) & 7u : 0u;
+    if (bulk_pending) {  // the previous tile's bulk copy must have read the staging
+      if (lane == 0) bulk_read_wait();
+      __syncwarp();
+      bulk_pending = false;
+    }
     if (fits && c) {
       SR r;
       r.init(base_s, e);
@@ -1074,10 +1113,8 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     }
     const unsigned long long P = Pc + toff;
     if (fits) {
-#ifndef BH_X_NOFLUSH
-      if (aligned) flush_aligned_stg(a.out, a.nsym, P, C, stg_s);
+      if (aligned) bulk_pending = flush_bulk(a.out, a.nsym, P, C, stg_s);
       else flush_compact(a.out, a.nsym, P, C, stg_s);
-#endif
     } else {
       // reference rounds (staging.py:123-146) with capacity cap - 8
       const bool active = lane < nsl;
@@ -1121,6 +1158,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     buf ^= 1;
   }
   cp_wait<0>();
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // bulk stores complete
   if (!have_off) mbar_wait(bar_off, 0);  // keep warp 0's arrival inside the CTA's lifetime
   if (__any_sync(0xffffffffu, bad) && lane == 0) tag_status(a.rep, ep, BH_INVALID);
   MARK(TRACE_SLOTS - 2);
