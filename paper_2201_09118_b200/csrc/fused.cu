@@ -45,7 +45,17 @@
 namespace bh {
 
 constexpr int HALO_WORDS = 8;
-constexpr int FUSED_MAX_THREADS = 768;  // <= 24 warps: up to 85 registers per thread
+#ifndef BH_MAXW
+#define BH_MAXW 24
+#endif
+#ifndef BH_CAPF
+#define BH_CAPF 1.12
+#endif
+#ifndef BH_CAPADD
+#define BH_CAPADD 96
+#endif
+constexpr int FUSED_MAX_WARPS = BH_MAXW;
+constexpr int FUSED_MAX_THREADS = 32 * FUSED_MAX_WARPS;  // 24 warps: up to 85 registers per thread
 constexpr uint32_t NEED_STAGED = 9;  // BH_NEED_STAGED
 
 // descriptor: [63:38] epoch (26 bits) | [37:36] flags | [35:0] value
@@ -165,17 +175,24 @@ __device__ __forceinline__ uint32_t lds32_if(uint32_t a, uint32_t p, uint32_t v)
 // predicated load of the word after next -- no branch, and the loaded word is
 // only needed one advance later, so shared-memory latency stays off the
 // decode chain.
+// Staged tile words are skewed by one word per 32 (logical word j sits at
+// physical word j + j/32): lanes read words about four apart (128-bit
+// subsequences), which would put lanes l, l+8, l+16 and l+24 on one bank.
+__device__ __forceinline__ uint32_t skew_addr(uint32_t base_s, uint32_t j) { return base_s + ((j + (j >> 5)) << 2); }
+
 struct SR {
   uint32_t w0, w1, w2;  // MSB-first words at the cursor
   uint32_t off;         // bit offset into w0 (0..31)
-  uint32_t wa;          // shared address of the word after w2
+  uint32_t wi;          // logical index of the word after w2
+  uint32_t base;        // shared address of the tile buffer
   __device__ __forceinline__ void init(uint32_t base_s, uint32_t rel) {
-    const uint32_t a = base_s + ((rel >> 5) << 2);
-    w0 = lds32(a);
-    w1 = lds32(a + 4);
-    w2 = lds32(a + 8);
+    const uint32_t j = rel >> 5;
+    base = base_s;
+    w0 = lds32(skew_addr(base_s, j));
+    w1 = lds32(skew_addr(base_s, j + 1));
+    w2 = lds32(skew_addr(base_s, j + 2));
     off = rel & 31;
-    wa = a + 12;
+    wi = j + 3;
   }
   __device__ __forceinline__ uint32_t peek() const { return __funnelshift_l(w1, w0, off); }
   __device__ __forceinline__ void skip(uint32_t n) {  // n <= 32
@@ -183,8 +200,8 @@ struct SR {
     const uint32_t adv = t >> 5;
     w0 = adv ? w1 : w0;
     w1 = adv ? w2 : w1;
-    wa += adv << 2;
-    w2 = lds32(wa - 4);  // the word after w1 (unchanged when adv == 0): no branch
+    wi += adv;
+    w2 = lds32(skew_addr(base, wi - 1));  // the word after w1 (unchanged when adv == 0): no branch
     off = t & 31;
   }
 };
@@ -447,9 +464,11 @@ __device__ __forceinline__ uint64_t stage_words(const FusedArgs& a, uint64_t til
   uint64_t w1 = ((s0 + a.seq_bits) >> 5) + HALO_WORDS;
   w1 = (w1 + 3) & ~3ull;
   if (w1 > a.words_alloc) w1 = a.words_alloc;
-  const uint32_t nch = (uint32_t)((w1 - w0) >> 2);
-  for (uint32_t c = lane; c < nch; c += 32) cp_async16(buf + 4 * c, a.words + w0 + 4 * c);
-  return w0 * 32;  // bit offset of buf[0]
+  const uint32_t nw = (uint32_t)(w1 - w0);
+  const uint32_t bs = smem_u32(buf);
+  for (uint32_t j = lane; j < nw; j += 32)  // word by word into the skewed layout (skew_addr)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(skew_addr(bs, j)), "l"(a.words + w0 + j) : "memory");
+  return w0 * 32;  // bit offset of logical word 0
 }
 
 // halfwords [sh, sh+8) of the 16 halfwords A||B (little-endian halfword order)
@@ -1193,11 +1212,12 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   // words one tile can stage: its span (+1 for a straddle), the 16-byte
   // alignment of the first word (+3), the halo, rounded up to 16 bytes
   c.wpb = ((seq_bits + 31) / 32 + 1 + 3 + HALO_WORDS + 3) & ~3u;
+  c.wpb = (c.wpb + (c.wpb >> 5) + 1 + 3) & ~3u;  // physical words: one skew word per 32
   // staging sized from the header's compression ratio (no device round trip):
   // a tile emits about seq_bits * symbols / total_bits symbols; a tile above
   // the capacity takes the reference's rounds, so any value is correct
   const double per_bit = s->total_bits ? (double)s->symbol_count / (double)s->total_bits : 1.0;
-  uint32_t cap = (uint32_t)(seq_bits * per_bit * 1.12) + 96;
+  uint32_t cap = (uint32_t)(seq_bits * per_bit * BH_CAPF) + BH_CAPADD;
   if (env_int("BH_FUSED_CAP", 0)) cap = (uint32_t)env_int("BH_FUSED_CAP", 0);
   const uint32_t cmax = s->subseqs_per_seq * (s->subseq_bits + 31) + 16;
   if (cap > cmax) cap = cmax;
@@ -1225,11 +1245,11 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   c.per_warp = (uint32_t)align16(8 * (size_t)c.wpb + 2 * (size_t)c.cap + 32);
   int w = env_int("BH_FUSED_WARPS", 0);
   if (w <= 0) {
-    w = (int)((220 * 1024 - c.tables) / c.per_warp);
-    if (w > 24) w = 24;
+    w = (int)((223 * 1024 - c.tables) / c.per_warp);
+    if (w > FUSED_MAX_WARPS) w = FUSED_MAX_WARPS;
     if (w < 1) w = 1;
   }
-  if (w > 24) w = 24;
+  if (w > FUSED_MAX_WARPS) w = FUSED_MAX_WARPS;
   // small inputs: fewer warps per CTA so that every SM gets a group
   static int sms = 0;
   if (!sms) {
