@@ -98,6 +98,7 @@ struct FusedArgs {
   uint32_t first_entry;  // bh_stream.first_entry
   uint32_t wide;         // table layout: 1 = wlut12, 0 = replicated wlut8 (+ lut12 if has_l12)
   uint32_t t_lim, t_c12, t_wp, t_l12;  // shared-memory table offsets (bytes)
+  uint32_t t_ljs, ljs_bytes;            // shared copy of ljsym for the limit search (0 bytes: global)
   unsigned long long* trace;  // debug timeline (TR instantiation only)
 };
 
@@ -212,6 +213,7 @@ struct FTab {
   uint32_t dst;    // entry stride shift: 7 (8 replicas x 16 B) or 4 (16 B)
   uint32_t l12;    // shared address of lut12
   uint32_t c12;    // shared address of clut12
+  uint32_t ljs;    // shared address of the canonical symbol order (0: read it from global)
   uint32_t lim;    // shared address of lim (u64[33])
   uint32_t base;   // shared address of base (i64[33])
   TableView t;
@@ -220,7 +222,8 @@ struct FTab {
 
 // one codeword from a 32-bit window when the 8-bit table cannot answer
 __device__ __noinline__ uint32_t fslow(uint32_t win, const uint32_t lim_s, const uint32_t base_s,
-                                       const uint16_t* __restrict__ ljsym, uint32_t kind, TableView t) {
+                                       const uint16_t* __restrict__ ljsym, uint32_t kind, TableView t,
+                                       uint32_t ljs_s) {
   if (kind == 0) {
     const uint2 l32 = lds64(lim_s + 32 * 8);
     if ((unsigned long long)win >= (((unsigned long long)l32.y << 32) | l32.x)) return 0;
@@ -232,7 +235,8 @@ __device__ __noinline__ uint32_t fslow(uint32_t win, const uint32_t lim_s, const
     }
     const uint2 bb = lds64(base_s + lo * 8);
     const long long idx = (long long)(((unsigned long long)bb.y << 32) | bb.x) + (long long)(win >> (32 - lo));
-    return (uint32_t)__ldg(ljsym + idx) | (lo << 16);
+    const uint32_t sym = ljs_s ? lds16(ljs_s + 2 * (uint32_t)idx) : (uint32_t)__ldg(ljsym + idx);
+    return sym | (lo << 16);
   }
   return slow_lookup(t, win);
 }
@@ -240,7 +244,7 @@ __device__ __noinline__ uint32_t fslow(uint32_t win, const uint32_t lim_s, const
 // a code longer than 8 bits: shared 12-bit table, else the limit search
 __device__ __forceinline__ uint32_t flong(uint32_t win, const FTab& T) {
   const uint32_t e = T.l12 ? lds32(T.l12 + ((win >> (32 - FB)) << 2)) : 0u;
-  return e ? e : fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t);
+  return e ? e : fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs);
 }
 
 // one codeword: sym | len<<16 (0 = no codeword matches)
@@ -264,7 +268,7 @@ __device__ __forceinline__ uint32_t clen(uint32_t win, const FTab& T) {
     const uint32_t m = y & 0xffeu;
     return m ? __ffs(m) - 1 : (y >> 12);
   }
-  return (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t) >> 16) & 0xffu;
+  return (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
 }
 
 // count codewords starting in [pos, stop) (tile-relative); pos ends at the exit.
@@ -280,7 +284,7 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
     const uint32_t b = y >> 12;
     if (pos + b <= stop) {
       if (!y) {  // first code longer than 12 bits
-        const uint32_t l = (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t) >> 16) & 0xffu;
+        const uint32_t l = (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
         if (!l) return false;
         n += 1;
         r.skip(l);
@@ -628,7 +632,8 @@ __device__ __forceinline__ void gap_window(const FusedArgs& a, uint64_t tile, ui
 template <int VAR>
 __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, uint64_t tile, uint32_t base_s,
                                             uint64_t wb0, uint32_t nsl, uint32_t ep, uint32_t& e, uint32_t& c,
-                                            bool& bad, int32_t seed_o = -1, uint32_t* cand_out = nullptr) {
+                                            bool& bad, int32_t seed_o = -1, uint32_t* cand_out = nullptr,
+                                            bool* fullfix = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t sb = a.sb;
   const uint64_t j0 = tile * a.sps;
@@ -688,6 +693,26 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
       indep = __all_sync(0xffffffffu, cand_x == x0);
     }
     const uint32_t xlast = __shfl_sync(0xffffffffu, x, nsl - 1);
+    if (seed_o < 0 && !indep) {
+      // The candidates disagree after the first slot: follow the candidate
+      // set through the next slots (lane j carries seed j) until it collapses
+      // onto the speculative chain.  Then the tile's exit is still
+      // seed-independent, but the slots before the collapse depend on the
+      // seed, so the tile is finished by a full re-synchronisation later.
+      uint32_t cx = cand_x;
+      for (uint32_t k = 1; k < nsl; ++k) {
+        const uint32_t ek = __shfl_sync(0xffffffffu, e, k), ck = __shfl_sync(0xffffffffu, c, k);
+        const uint32_t xk = __shfl_sync(0xffffffffu, x, k), sk = __shfl_sync(0xffffffffu, stop, k);
+        uint32_t cn, xn;
+        if (cx == 0xffffffffu || !resync(base_s, ek, ck, xk, cx, sk, T, cn, xn)) xn = 0xffffffffu;
+        cx = xn;
+        if (__all_sync(0xffffffffu, cx == xk)) {
+          indep = true;
+          if (fullfix) *fullfix = true;
+          break;
+        }
+      }
+    }
     if (seed_o < 0) {
       // speculative: publish the exit when it does not depend on the seed
       if (cand_out) *cand_out = cand_c;
@@ -813,6 +838,7 @@ __device__ unsigned long long lookback_wide(unsigned long long* desc, uint64_t c
 }
 
 constexpr uint32_t MAX_SMEM_TILES = 512;
+constexpr int32_t FULL_FIX = 0x7fffffff;  // tile_dlt marker: re-synchronise the whole tile in the fix-up
 
 template <int VAR, int TR>
 __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a) {
@@ -858,8 +884,9 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     mbar_init(bar_dt, 1);
     mbar_init(bar_off, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(bar_ct, T_LIMBASE + 2 * FB_SIZE);
+    mbar_expect_tx(bar_ct, T_LIMBASE + 2 * FB_SIZE + a.ljs_bytes);
     bulk_g2s(sm_s + a.t_c12, tb_ + L.clut12, 2 * FB_SIZE, bar_ct);
+    if (a.ljs_bytes) bulk_g2s(sm_s + a.t_ljs, tb_ + L.ljsym, a.ljs_bytes, bar_ct);
     bulk_g2s(sm_s + a.t_lim, tb_ + L.lim, T_LIMBASE, bar_ct);  // lim, base (contiguous)
     if (a.wide) {
       mbar_expect_tx(bar_dt, T_WIDE_DEC);
@@ -884,6 +911,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   T.base = sm_s + a.t_lim + 33 * 8;
   T.l12 = (!a.wide && a.has_l12) ? sm_s + a.t_l12 : 0u;
   T.c12 = sm_s + a.t_c12;
+  T.ljs = (a.ljs_bytes && hdr->kind == 0) ? sm_s + a.t_ljs : 0u;
   T.t = table_view(a.table, a.max_codes, hdr->ncodes);
   T.kind = hdr->kind;
   __syncthreads();  // barriers initialised
@@ -900,8 +928,12 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     __syncwarp();
     const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
     uint32_t e, c, cand = 0;
-    tile_counts<VAR>(a, T, tile, wbase_s + 4 * a.wpb * buf, wb_a, nsl, ep, e, c, bad, -1, &cand);
-    if (VAR == BH_VARIANT_SYNC) a.cand[tile * 32 + lane] = (uint16_t)min(cand, 0xffffu);
+    bool fullfix = false;
+    tile_counts<VAR>(a, T, tile, wbase_s + 4 * a.wpb * buf, wb_a, nsl, ep, e, c, bad, -1, &cand, &fullfix);
+    if (VAR == BH_VARIANT_SYNC) {
+      a.cand[tile * 32 + lane] = (uint16_t)min(cand, 0xffffu);
+      if (lane == 0) a.tile_dlt[tile] = fullfix ? FULL_FIX : 0;
+    }
     uint32_t incl = c;
     for (int off = 1; off < 32; off <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
@@ -936,8 +968,9 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       bool serial = false;
       if (mine && tk > 0) {
         unsigned long long dp, ds = ld_acquire(a.exit_desc + tk);
+        const bool ff = a.tile_dlt[tk] == FULL_FIX;
         while (!desc_ready(dp = ld_acquire(a.exit_desc + tk - 1), ep)) __nanosleep(32);
-        if ((ds & D_INC) && (dp & D_INC)) {
+        if ((ds & D_INC) && (dp & D_INC) && !ff) {
           const uint32_t o = (uint32_t)((dp & D_VAL) - tk * a.seq_bits);
           if (o >= 32) {
             bad = true;
@@ -967,7 +1000,8 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         dp = __shfl_sync(0xffffffffu, dp, 0);
         const uint32_t o = (uint32_t)((dp & D_VAL) - st * a.seq_bits);
         const unsigned long long ds = ld_acquire(a.exit_desc + st);
-        if (ds & D_INC) {  // seed-independent tile behind a dependent one
+        const bool ff = __shfl_sync(0xffffffffu, lane == 0 ? (uint32_t)(a.tile_dlt[st] == FULL_FIX) : 0u, 0) != 0;
+        if ((ds & D_INC) && !ff) {  // first-slot swap behind a dependent predecessor
           if (o >= 32) {
             bad = true;
           } else if (lane == 0) {
@@ -1203,7 +1237,7 @@ int env_int(const char* name, int dflt) {
 }
 
 struct FusedCfg {
-  uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12, wide, t_lim, t_c12, t_wp, t_l12;
+  uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12, wide, t_lim, t_c12, t_wp, t_l12, t_ljs, ljs_bytes;
 };
 
 FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
@@ -1241,6 +1275,11 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
     c.t_l12 = c.t_wp + 4096;
     c.tables = (uint32_t)align16(c.t_l12 + (c.has_l12 ? 4 * FB_SIZE : 0));
   }
+  // codes longer than the tables reach: the canonical symbol order in shared
+  // memory keeps the limit search off global memory (books up to 4096 codes)
+  c.ljs_bytes = (c.has_l12 && s->max_codes <= 4096) ? (uint32_t)align16(2 * (size_t)s->max_codes) : 0u;
+  c.t_ljs = c.tables;
+  c.tables += c.ljs_bytes;
   // two word buffers, staging
   c.per_warp = (uint32_t)align16(8 * (size_t)c.wpb + 2 * (size_t)c.cap + 32);
   int w = env_int("BH_FUSED_WARPS", 0);
@@ -1350,6 +1389,8 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.t_c12 = cfg.t_c12;
   a.t_wp = cfg.t_wp;
   a.t_l12 = cfg.t_l12;
+  a.t_ljs = cfg.t_ljs;
+  a.ljs_bytes = cfg.ljs_bytes;
   static int sms = 0;
   if (!sms) {
     int dev = 0;
