@@ -388,9 +388,16 @@ __device__ bool fdecode_global(SR& r, uint32_t c, uint16_t* out, uint64_t at, ui
 }
 
 // Re-decode a window from a new entry, walking the previous decode (entry eo,
-// count co, exit xo) in lock-step; once both cursors meet the rest is shared.
-__device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co, uint32_t xo, uint32_t en,
-                                       uint32_t stop, const FTab& T, uint32_t& cn, uint32_t& xn) {
+// count co, exit xo) in lock-step; once both cursors meet the rest is shared
+// (sync_decoder.py:90-101).  The lower cursor advances a whole 12-bit count
+// table entry at a time: its start mask says at once whether the other
+// cursor's position is one of its codeword starts (the parses meet there) or
+// lies between two of them, so no codeword is stepped singly except codes
+// longer than 12 bits.
+// Per-codeword lock-step walk: cheaper than the mask walk when a 12-bit entry
+// holds only a couple of codewords (long-code books, wide layout).
+__device__ __forceinline__ bool resync_step(uint32_t base_s, uint32_t eo, uint32_t co, uint32_t xo, uint32_t en,
+                                            uint32_t stop, const FTab& T, uint32_t& cn, uint32_t& xn) {
   uint32_t po = eo, pn = en, no = 0, nn = 0;
   SR ro, rn;
   ro.init(base_s, po);
@@ -411,6 +418,53 @@ __device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co
       pn += l;
       ++nn;
     }
+  }
+}
+
+__device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co, uint32_t xo, uint32_t en,
+                                       uint32_t stop, const FTab& T, uint32_t& cn, uint32_t& xn) {
+  if (T.dsh != 24) return resync_step(base_s, eo, co, xo, en, stop, T, cn, xn);  // wide layout
+  uint32_t po = eo, pn = en, no = 0, nn = 0;
+  SR ro, rn;
+  ro.init(base_s, po);
+  rn.init(base_s, pn);
+  const uint32_t ct = T.c12;
+  while (true) {
+    if (pn >= stop) { cn = nn; xn = pn; return true; }
+    if (po == pn) { cn = nn + (co - no); xn = xo; return true; }
+    const bool old_low = po < pn;
+    SR& r = old_low ? ro : rn;
+    const uint32_t win = r.peek();
+    const uint32_t y = lds16(ct + ((win >> (32 - FB)) << 1));
+    if (!y) {  // a code longer than 12 bits: one codeword
+      const uint32_t l = (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
+      if (!l) return false;
+      r.skip(l);
+      if (old_low) { po += l; ++no; } else { pn += l; ++nn; }
+      continue;
+    }
+    const uint32_t mask = y & 0xfffu, b = y >> 12;
+    const uint32_t lo = old_low ? po : pn, d = old_low ? pn - po : po - pn;  // d >= 1
+    const uint32_t rem = old_low ? 0xffffu : stop - pn;                     // new parse: room to stop
+    uint32_t adv, cnt;
+    if (d < b && ((mask >> d) & 1u) && d < rem) {  // the lower parse has a start where the other is
+      adv = d;
+      cnt = __popc(mask & ((1u << d) - 1u));
+    } else if (rem < b) {  // new parse: the window ends inside this entry
+      cnt = __popc(mask & ((1u << rem) - 1u));
+      const uint32_t hi = mask >> rem;
+      adv = hi ? rem + __ffs(hi) - 1 : b;
+    } else if (d < b) {  // steps over the other cursor: stop at the first start after it
+      const uint32_t hi = mask >> d;
+      adv = hi ? d + __ffs(hi) - 1 : b;
+      cnt = __popc(mask & ((1u << adv) - 1u));
+    } else {
+      adv = b;
+      cnt = __popc(mask);
+    }
+    (void)lo;
+    r.skip(adv);
+    if (old_low) { po += adv; no += cnt; } else { pn += adv; nn += cnt; }
   }
 }
 
