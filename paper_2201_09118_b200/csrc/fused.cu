@@ -218,6 +218,7 @@ struct FTab {
   uint32_t base;   // shared address of base (i64[33])
   TableView t;
   uint32_t kind;
+  uint32_t max_len;  // longest code length of the book (seed candidates)
 };
 
 // one codeword from a 32-bit window when the 8-bit table cannot answer
@@ -743,7 +744,11 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
     uint32_t cand_c = c0, cand_x = x0;
     bool indep = true;
     if (tile > 0) {
-      if (!resync(base_s, b0, c0, x0, b0 + lane, stop0, T, cand_c, cand_x)) cand_x = 0xffffffffu;
+      // the true seed lies within the codeword straddling the boundary, so
+      // only offsets below the longest code length are candidates
+      if (lane < T.max_len) {
+        if (!resync(base_s, b0, c0, x0, b0 + lane, stop0, T, cand_c, cand_x)) cand_x = 0xffffffffu;
+      }
       indep = __all_sync(0xffffffffu, cand_x == x0);
     }
     const uint32_t xlast = __shfl_sync(0xffffffffu, x, nsl - 1);
@@ -968,6 +973,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   T.ljs = (a.ljs_bytes && hdr->kind == 0) ? sm_s + a.t_ljs : 0u;
   T.t = table_view(a.table, a.max_codes, hdr->ncodes);
   T.kind = hdr->kind;
+  T.max_len = hdr->max_len ? min(hdr->max_len, 32u) : 32u;
   __syncthreads();  // barriers initialised
   mbar_wait(bar_ct, 0);
   MARK(1);
