@@ -93,3 +93,18 @@ def test_fused_matches_staged_on_layouts(ph):
             st = ph.encode(syms, ph.book_for(syms, width), ph.LayoutConfig(*lay), with_gap=True)
             assert np.array_equal(ph.gap_decoder.decode(st), syms), lay
             assert np.array_equal(ph.sync_decoder.decode(st), syms), lay
+
+
+@pytest.mark.parametrize("wide", ["", "0", "1"])
+@pytest.mark.parametrize("sigma,eps", [(0.2, 1e-3), (0.6, 0.0), (3.0, 0.0), (8.0, 0.0), (22.0, 0.0), (8.0, 2e-3)])
+def test_table_layouts_on_cusz_fields(ph, monkeypatch, wide, sigma, eps):
+    """Both decode-table layouts (narrow 8-bit replicated / wide 12-bit) and
+    the automatic choice decode cuSZ-shaped fields bit-exactly -- short and
+    long codes, seed-dependent seams (sigma 22), codes past 12 bits (eps)."""
+    from paper_2201_09118_b200.synth import gaussian_codes
+    if wide:
+        monkeypatch.setenv("BH_FUSED_WIDE", wide)
+    codes = gaussian_codes(1_500_000, 1024, sigma, eps, seed=int(sigma * 10) + 3)
+    st = ph.encode(codes, ph.book_for(codes, 16), ph.DEFAULT_LAYOUT, with_gap=True)
+    assert np.array_equal(ph.gap_decoder.decode(st), codes)
+    assert np.array_equal(ph.sync_decoder.decode(st), codes)
