@@ -280,30 +280,37 @@ __device__ __forceinline__ uint32_t clen(uint32_t win, const FTab& T) {
 __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, const FTab& T, uint32_t& n) {
   const uint32_t ct = pin(T.c12);
   while (pos < stop) {
-    const uint32_t win = r.peek();
-    const uint32_t y = lds16(ct + ((win >> (32 - FB)) << 1));
-    const uint32_t b = y >> 12;
-    if (pos + b <= stop) {
-      if (!y) {  // first code longer than 12 bits
-        const uint32_t l = (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
-        if (!l) return false;
-        n += 1;
-        r.skip(l);
-        pos += l;
-        continue;
-      }
+    // tight loop: whole entries that end at or before the window end
+#pragma unroll 2
+    while (true) {
+      const uint32_t y = lds16(ct + ((r.peek() >> (32 - FB)) << 1));
+      const uint32_t b = y >> 12;
+      if (y == 0 || pos + b > stop) break;
       n += __popc(y & 0xfffu);
       r.skip(b);
       pos += b;
-    } else {  // the window ends inside this entry (stop - pos < b <= 12)
-      const uint32_t rem = stop - pos;
-      const uint32_t mask = y & 0xfffu;
-      n += __popc(mask & ((1u << rem) - 1u));
-      const uint32_t hi = mask >> rem;
-      const uint32_t adv = hi ? rem + __ffs(hi) - 1 : b;
-      r.skip(adv);
-      pos += adv;
+      if (pos >= stop) break;
     }
+    if (pos >= stop) break;
+    const uint32_t win = r.peek();
+    const uint32_t y = lds16(ct + ((win >> (32 - FB)) << 1));
+    if (!y) {  // first code longer than 12 bits
+      const uint32_t l = (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
+      if (!l) return false;
+      n += 1;
+      r.skip(l);
+      pos += l;
+      continue;
+    }
+    // the window ends inside this entry (stop - pos < b <= 12)
+    const uint32_t b = y >> 12;
+    const uint32_t rem = stop - pos;
+    const uint32_t mask = y & 0xfffu;
+    n += __popc(mask & ((1u << rem) - 1u));
+    const uint32_t hi = mask >> rem;
+    const uint32_t adv = hi ? rem + __ffs(hi) - 1 : b;
+    r.skip(adv);
+    pos += adv;
   }
   return true;
 }
@@ -316,39 +323,29 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
 __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const FTab& T) {
   const uint32_t wl = pin(T.wl), dsh = T.dsh, dstr = T.dst;
   int32_t k = (int32_t)c;
-#if !defined(BH_FDEC_PRED)
-  while (k >= 7) {
-    const uint32_t win = r.peek();
-    const uint4 w = lds128(wl + ((win >> dsh) << dstr));
-    if (w.w) {
-      // one halfword store, then three aligned word stores: an odd start
-      // shifts the entry by one halfword (the seventh halfword written is
-      // garbage inside the lane's own range, overwritten by its next store)
+  while (k > 0) {
+    // tight loop: whole entries while at least seven symbols remain; one
+    // halfword store, then three aligned word stores (an odd start shifts the
+    // entry by one halfword; the seventh halfword written is garbage inside
+    // the lane's own range, overwritten by its next store)
+#pragma unroll 2
+    while (k >= 7) {
+      const uint4 w = lds128(wl + ((r.peek() >> dsh) << dstr));
+      if (!w.w) break;  // a code the table does not hold: one entry below
       const uint32_t odd = dst & 2u;
       const uint32_t sel = odd ? 0x5432u : 0x3210u;
       const uint32_t a4 = (dst & ~3u) + (odd << 1);
-#ifndef BH_X_NOSTORE
       sts16(dst, w.x);
       sts32(a4, __byte_perm(w.x, w.y, sel));
       sts32(a4 + 4, __byte_perm(w.y, w.z, sel));
       sts32(a4 + 8, __byte_perm(w.z, w.z, sel));
-#endif
       const int32_t n = (int32_t)((w.w >> 4) & 15u);
       dst += (uint32_t)n << 1;
       k -= n;
       r.skip(w.w & 15u);
-    } else {
-      const uint32_t e = flong(win, T);
-      const uint32_t len = (e >> 16) & 0xffu;
-      if (!len) return false;
-      sts16(dst, e);
-      dst += 2;
-      k -= 1;
-      r.skip(len);
     }
-  }
-#endif
-  while (k > 0) {
+    if (k <= 0) break;
+    // one entry with predicated stores: the last few symbols, or a long code
     const uint32_t win = r.peek();
     const uint4 w = lds128(wl + ((win >> dsh) << dstr));
     if (w.w) {
