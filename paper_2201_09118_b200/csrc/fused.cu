@@ -45,6 +45,10 @@
 namespace bh {
 
 constexpr int HALO_WORDS = 8;
+#ifndef BH_UNR
+#define BH_UNR 4
+#endif
+constexpr int kUnroll = BH_UNR;  // unroll of the tight count/decode loops
 #ifndef BH_MAXW
 #define BH_MAXW 24
 #endif
@@ -281,7 +285,7 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
   const uint32_t ct = pin(T.c12);
   while (pos < stop) {
     // tight loop: whole entries that end at or before the window end
-#pragma unroll 2
+#pragma unroll (kUnroll)
     while (true) {
       const uint32_t y = lds16(ct + ((r.peek() >> (32 - FB)) << 1));
       const uint32_t b = y >> 12;
@@ -328,7 +332,7 @@ __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const F
     // halfword store, then three aligned word stores (an odd start shifts the
     // entry by one halfword; the seventh halfword written is garbage inside
     // the lane's own range, overwritten by its next store)
-#pragma unroll 2
+#pragma unroll (kUnroll)
     while (k >= 7) {
       const uint4 w = lds128(wl + ((r.peek() >> dsh) << dstr));
       if (!w.w) break;  // a code the table does not hold: one entry below
