@@ -689,7 +689,7 @@ template <int VAR>
 __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, uint64_t tile, uint32_t base_s,
                                             uint64_t wb0, uint32_t nsl, uint32_t ep, uint32_t& e, uint32_t& c,
                                             bool& bad, int32_t seed_o = -1, uint32_t* cand_out = nullptr,
-                                            bool* fullfix = nullptr) {
+                                            bool* fullfix = nullptr, const uint32_t* gpre = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t sb = a.sb;
   const uint64_t j0 = tile * a.sps;
@@ -701,9 +701,10 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
   e = b;
   c = 0;
   if (VAR == BH_VARIANT_GAP) {
-    const uint32_t g = active ? a.gap[j] : 0u;
+    // gpre: this lane's gap byte and lane 31's successor, prefetched by the caller
+    const uint32_t g = gpre ? gpre[0] : (active ? a.gap[j] : 0u);
     uint32_t gn = __shfl_down_sync(0xffffffffu, g, 1);
-    if (lane == nsl - 1) gn = (j + 1 < a.nsub) ? a.gap[j + 1] : 0u;
+    if (lane == nsl - 1) gn = gpre && nsl == 32 ? gpre[1] : ((j + 1 < a.nsub) ? a.gap[j + 1] : 0u);
     e = b + g;
     stop = (j + 1 < a.nsub) ? b + sb + gn : tbr;
     if (stop > tbr) stop = tbr;
@@ -981,16 +982,30 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
 
   // ---- phase 1: count ----------------------------------------------------
   uint32_t buf = 0;
+  // GAP: the gap bytes of a tile are loaded one tile ahead, like its words
+  auto gap_load = [&](uint64_t t, uint32_t* g) {
+    const uint64_t j = t * a.sps + lane;
+    g[0] = (lane < a.sps && j < a.nsub) ? a.gap[j] : 0u;
+    g[1] = (lane == 31 && t * a.sps + 32 < a.nsub) ? a.gap[t * a.sps + 32] : 0u;
+  };
+  uint32_t gcur[2] = {0, 0}, gnext[2] = {0, 0};
+  if (VAR == BH_VARIANT_GAP && tile < t1) gap_load(tile, gcur);
   for (; tile < t1; tile += W) {
     const uint64_t tn = tile + W;
-    if (tn < t1) wb_b = stage_words(a, tn, wbase + (buf ^ 1) * a.wpb);
+    if (tn < t1) {
+      wb_b = stage_words(a, tn, wbase + (buf ^ 1) * a.wpb);
+      if (VAR == BH_VARIANT_GAP) gap_load(tn, gnext);
+    }
     cp_commit();
     cp_wait<1>();
     __syncwarp();
     const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
     uint32_t e, c, cand = 0;
     bool fullfix = false;
-    tile_counts<VAR>(a, T, tile, wbase_s + 4 * a.wpb * buf, wb_a, nsl, ep, e, c, bad, -1, &cand, &fullfix);
+    tile_counts<VAR>(a, T, tile, wbase_s + 4 * a.wpb * buf, wb_a, nsl, ep, e, c, bad, -1, &cand, &fullfix,
+                     VAR == BH_VARIANT_GAP && a.sps == 32 ? gcur : nullptr);
+    gcur[0] = gnext[0];
+    gcur[1] = gnext[1];
     if (VAR == BH_VARIANT_SYNC) {
       a.cand[tile * 32 + lane] = (uint16_t)min(cand, 0xffffu);
       if (lane == 0) a.tile_dlt[tile] = fullfix ? FULL_FIX : 0;
