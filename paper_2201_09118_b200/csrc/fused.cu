@@ -126,6 +126,18 @@ __device__ __forceinline__ void tag_status(DevReport* rep, uint32_t ep, uint32_t
   atomicMax(&rep->pad[0], v);  // pad[0] = tagged status (see bh_report_read)
 }
 
+// Descriptors carry their value in the 64-bit word itself (epoch | flags |
+// value), so readers need no ordering beyond the word: relaxed gpu-scope
+// accesses avoid the release/acquire fences on the look-back's critical path.
+__device__ __forceinline__ void st_relaxed(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
 // ---- shared-memory primitives (explicit 32-bit shared addresses) ----------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
@@ -517,18 +529,32 @@ template <int N>
 __device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 // stage the words of `tile` (16 B chunks, one per lane per step)
-__device__ __forceinline__ uint64_t stage_words(const FusedArgs& a, uint64_t tile, uint32_t* buf) {
+// Stage a tile's words: 16-byte cp.async chunks into the warp's landing
+// buffer (few, wide L2 requests); skew_in() then spreads them into the skewed
+// decode buffer.  Returns the bit offset of logical word 0.
+__device__ __forceinline__ uint64_t stage_words(const FusedArgs& a, uint64_t tile, uint32_t* land, uint32_t& nch) {
   const uint32_t lane = threadIdx.x & 31;
   const uint64_t s0 = tile * (uint64_t)a.seq_bits;
   const uint64_t w0 = (s0 >> 5) & ~3ull;
   uint64_t w1 = ((s0 + a.seq_bits) >> 5) + HALO_WORDS;
   w1 = (w1 + 3) & ~3ull;
   if (w1 > a.words_alloc) w1 = a.words_alloc;
-  const uint32_t nw = (uint32_t)(w1 - w0);
-  const uint32_t bs = smem_u32(buf);
-  for (uint32_t j = lane; j < nw; j += 32)  // word by word into the skewed layout (skew_addr)
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(skew_addr(bs, j)), "l"(a.words + w0 + j) : "memory");
-  return w0 * 32;  // bit offset of logical word 0
+  nch = (uint32_t)((w1 - w0) >> 2);
+  for (uint32_t c = lane; c < nch; c += 32) cp_async16(land + 4 * c, a.words + w0 + 4 * c);
+  return w0 * 32;
+}
+
+// landing buffer (contiguous) -> decode buffer (skew_addr layout); the caller
+// waits for the cp.async group and syncs the warp on both sides
+__device__ __forceinline__ void skew_in(uint32_t land_s, uint32_t buf_s, uint32_t nch) {
+  const uint32_t lane = threadIdx.x & 31;
+  for (uint32_t c = lane; c < nch; c += 32) {
+    const uint4 v = lds128(land_s + 16 * c);
+    sts32(skew_addr(buf_s, 4 * c), v.x);
+    sts32(skew_addr(buf_s, 4 * c + 1), v.y);
+    sts32(skew_addr(buf_s, 4 * c + 2), v.z);
+    sts32(skew_addr(buf_s, 4 * c + 3), v.w);
+  }
 }
 
 // halfwords [sh, sh+8) of the 16 halfwords A||B (little-endian halfword order)
@@ -777,7 +803,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
     if (seed_o < 0) {
       // speculative: publish the exit when it does not depend on the seed
       if (cand_out) *cand_out = cand_c;
-      if (lane == 0) st_release(a.exit_desc + tile, mkdesc(ep, indep ? D_INC : D_AGG, indep ? wb0 + xlast : 0));
+      if (lane == 0) st_relaxed(a.exit_desc + tile, mkdesc(ep, indep ? D_INC : D_AGG, indep ? wb0 + xlast : 0));
 #ifdef BH_X_DEPSTAT
       if (lane == 0 && !indep) atomicAdd(&a.rep->pad[3], 1ull);
       if (lane == 0 && tile > 0) atomicAdd(&a.rep->pad[3], 1ull << 32);
@@ -808,7 +834,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
         }
       }
       const uint32_t xl = __shfl_sync(0xffffffffu, x, nsl - 1);
-      if (lane == 0) st_release(a.exit_desc + tile, mkdesc(ep, D_INC, wb0 + xl));
+      if (lane == 0) st_relaxed(a.exit_desc + tile, mkdesc(ep, D_INC, wb0 + xl));
     }
   }
   if (!active) c = 0;
@@ -860,10 +886,12 @@ __device__ __forceinline__ unsigned long long gtime() {
 
 // exclusive prefix of CTA `c` over the epoch-tagged CTA descriptors: every
 // predecessor descriptor is loaded in one round (lane l takes c-1-l, c-33-l..)
-__device__ unsigned long long lookback_wide(unsigned long long* desc, uint64_t c, uint32_t ep) {
+__device__ unsigned long long lookback_wide(unsigned long long* desc, uint64_t c, uint32_t ep,
+                                            unsigned long long* dbg = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   unsigned long long excl = 0;
   int64_t hi = (int64_t)c - 1;
+  uint32_t polls = 0;
   while (hi >= 0) {
     // up to 4 x 32 predecessors per round
     unsigned long long d[4];
@@ -873,11 +901,14 @@ __device__ unsigned long long lookback_wide(unsigned long long* desc, uint64_t c
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const int64_t idx = hi - (int64_t)lane - 32 * q;
-        d[q] = idx >= 0 ? ld_acquire(desc + idx) : mkdesc(ep, D_INC, 0);
+        d[q] = idx >= 0 ? ld_relaxed(desc + idx) : mkdesc(ep, D_INC, 0);
         ready = ready && desc_ready(d[q], ep);
       }
+      ++polls;
+      if (dbg && polls == 1 && lane == 0) dbg[0] = gtime();
       if (!__all_sync(0xffffffffu, ready)) __nanosleep(32); else break;
     } while (true);
+    if (dbg && lane == 0) { dbg[1] = gtime(); dbg[2] = polls; }
     // nearest inclusive descriptor (smallest distance) ends the walk
     uint32_t stop_q = 4, stop_lane = 32;
 #pragma unroll
@@ -960,9 +991,14 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       if (a.has_l12) bulk_g2s(sm_s + a.t_l12, tb_ + L.lut12, 4 * FB_SIZE, bar_dt);
     }
   }
+  // per warp: a landing buffer for the cp.async chunks of the next tile and
+  // the skewed decode buffer of the current one
+  uint32_t* const land = wbase;
+  const uint32_t land_s = wbase_s, dbuf_s = wbase_s + 4 * a.wpb;
   uint64_t tile = t0 + wib;
   uint64_t wb_a = 0, wb_b = 0;
-  if (tile < t1) wb_a = stage_words(a, tile, wbase);
+  uint32_t nch_a = 0, nch_b = 0;
+  if (tile < t1) wb_a = stage_words(a, tile, land, nch_a);
   cp_commit();
   FTab T;
   T.wl = a.wide ? sm_s : sm_s + 16 * (lane & 7);
@@ -981,7 +1017,6 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   MARK(1);
 
   // ---- phase 1: count ----------------------------------------------------
-  uint32_t buf = 0;
   // GAP: the gap bytes of a tile are loaded one tile ahead, like its words
   auto gap_load = [&](uint64_t t, uint32_t* g) {
     const uint64_t j = t * a.sps + lane;
@@ -992,17 +1027,19 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   if (VAR == BH_VARIANT_GAP && tile < t1) gap_load(tile, gcur);
   for (; tile < t1; tile += W) {
     const uint64_t tn = tile + W;
-    if (tn < t1) {
-      wb_b = stage_words(a, tn, wbase + (buf ^ 1) * a.wpb);
+    cp_wait<0>();  // this tile's words have landed
+    __syncwarp();
+    skew_in(land_s, dbuf_s, nch_a);
+    __syncwarp();
+    if (tn < t1) {  // the next tile's words land while this one is counted
+      wb_b = stage_words(a, tn, land, nch_b);
       if (VAR == BH_VARIANT_GAP) gap_load(tn, gnext);
     }
     cp_commit();
-    cp_wait<1>();
-    __syncwarp();
     const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
     uint32_t e, c, cand = 0;
     bool fullfix = false;
-    tile_counts<VAR>(a, T, tile, wbase_s + 4 * a.wpb * buf, wb_a, nsl, ep, e, c, bad, -1, &cand, &fullfix,
+    tile_counts<VAR>(a, T, tile, dbuf_s, wb_a, nsl, ep, e, c, bad, -1, &cand, &fullfix,
                      VAR == BH_VARIANT_GAP && a.sps == 32 ? gcur : nullptr);
     gcur[0] = gnext[0];
     gcur[1] = gnext[1];
@@ -1024,7 +1061,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       else a.tile_cnt[tile] = incl;
     }
     wb_a = wb_b;
-    buf ^= 1;
+    nch_a = nch_b;
   }
   cp_wait<0>();
   if (VAR == BH_VARIANT_SYNC) {
@@ -1043,9 +1080,9 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       if (!__any_sync(0xffffffffu, mine)) break;
       bool serial = false;
       if (mine && tk > 0) {
-        unsigned long long dp, ds = ld_acquire(a.exit_desc + tk);
+        unsigned long long dp, ds = ld_relaxed(a.exit_desc + tk);
         const bool ff = a.tile_dlt[tk] == FULL_FIX;
-        while (!desc_ready(dp = ld_acquire(a.exit_desc + tk - 1), ep)) __nanosleep(32);
+        while (!desc_ready(dp = ld_relaxed(a.exit_desc + tk - 1), ep)) __nanosleep(32);
         if ((ds & D_INC) && (dp & D_INC) && !ff) {
           const uint32_t o = (uint32_t)((dp & D_VAL) - tk * a.seq_bits);
           if (o >= 32) {
@@ -1072,10 +1109,10 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         const uint64_t st = t0 + wib + (kb + j) * W;
         unsigned long long dp = 0;
         if (lane == 0)
-          while (!((dp = ld_acquire(a.exit_desc + st - 1)) & D_INC) || !desc_ready(dp, ep)) __nanosleep(32);
+          while (!((dp = ld_relaxed(a.exit_desc + st - 1)) & D_INC) || !desc_ready(dp, ep)) __nanosleep(32);
         dp = __shfl_sync(0xffffffffu, dp, 0);
         const uint32_t o = (uint32_t)((dp & D_VAL) - st * a.seq_bits);
-        const unsigned long long ds = ld_acquire(a.exit_desc + st);
+        const unsigned long long ds = ld_relaxed(a.exit_desc + st);
         const bool ff = __shfl_sync(0xffffffffu, lane == 0 ? (uint32_t)(a.tile_dlt[st] == FULL_FIX) : 0u, 0) != 0;
         if ((ds & D_INC) && !ff) {  // first-slot swap behind a dependent predecessor
           if (o >= 32) {
@@ -1091,13 +1128,16 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
           continue;
         }
         // dependent tile: stage its words again and synchronise from the seed
-        const uint64_t wbs = stage_words(a, st, wbase);
+        uint32_t nchs;
+        const uint64_t wbs = stage_words(a, st, land, nchs);
         cp_commit();
         cp_wait<0>();
         __syncwarp();
+        skew_in(land_s, dbuf_s, nchs);
+        __syncwarp();
         const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - st * a.sps);
         uint32_t e, c;
-        tile_counts<VAR>(a, T, st, wbase_s, wbs, nsl, ep, e, c, bad, (int32_t)min(o, 255u));
+        tile_counts<VAR>(a, T, st, dbuf_s, wbs, nsl, ep, e, c, bad, (int32_t)min(o, 255u));
         uint32_t incl = c;
         for (int off = 1; off < 32; off <<= 1) {
           const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
@@ -1166,11 +1206,13 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   if (wib == 0) {
     unsigned long long excl = 0;
     if (cta == 0) {
-      if (lane == 0) st_release(a.cnt_desc, mkdesc(ep, D_INC, carry));
+      if (lane == 0) st_relaxed(a.cnt_desc, mkdesc(ep, D_INC, carry));
     } else {
-      if (lane == 0) st_release(a.cnt_desc + cta, mkdesc(ep, D_AGG, carry));
-      excl = lookback_wide(a.cnt_desc, cta, ep);
-      if (lane == 0) st_release(a.cnt_desc + cta, mkdesc(ep, D_INC, excl + carry));
+      if (lane == 0) st_relaxed(a.cnt_desc + cta, mkdesc(ep, D_AGG, carry));
+      MARK(5);
+      excl = lookback_wide(a.cnt_desc, cta, ep,
+                           TR ? a.trace + ((size_t)blockIdx.x * a.warps) * TRACE_SLOTS + 6 : nullptr);
+      if (lane == 0) st_relaxed(a.cnt_desc + cta, mkdesc(ep, D_INC, excl + carry));
     }
     if (lane == 0) {
       s_ctaoff = excl;
@@ -1185,15 +1227,12 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
 
   // ---- phase 2: decode and write -----------------------------------------
   tile = t0 + wib;
-  buf = 0;
-  if (tile < t1) wb_a = stage_words(a, tile, wbase);
+  if (tile < t1) wb_a = stage_words(a, tile, land, nch_a);
   cp_commit();
   bool have_off = false, bulk_pending = false;
   unsigned long long Pc = 0;
   for (; tile < t1; tile += W) {
     const uint64_t tn = tile + W;
-    if (tn < t1) wb_b = stage_words(a, tn, wbase + (buf ^ 1) * a.wpb);
-    cp_commit();
     const uint32_t info = a.lane_info[tile * 32 + lane];
     uint32_t C, toff;
     if (nt <= MAX_SMEM_TILES) {
@@ -1206,10 +1245,14 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       C = a.tile_cnt[tile];
       toff = a.tile_off[tile];
     }
-    cp_wait<1>();
+    cp_wait<0>();  // this tile's words have landed
     __syncwarp();
+    skew_in(land_s, dbuf_s, nch_a);
+    __syncwarp();
+    if (tn < t1) wb_b = stage_words(a, tn, land, nch_b);  // lands while this tile decodes
+    cp_commit();
     const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
-    const uint32_t base_s = wbase_s + 4 * a.wpb * buf;
+    const uint32_t base_s = dbuf_s;
     const uint32_t b = (uint32_t)((tile * a.sps + lane) * a.sb - wb_a);
     const uint32_t e = b + (info & 0xffffu);
     uint32_t o = info >> 16;
@@ -1236,6 +1279,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
 
     const bool aligned = have_off;
     if (!have_off) {
+      MARK(4);
       mbar_wait(bar_off, 0);
       Pc = *(volatile unsigned long long*)&s_ctaoff;
       have_off = true;
@@ -1284,7 +1328,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     }
     __syncwarp();
     wb_a = wb_b;
-    buf ^= 1;
+    nch_a = nch_b;
   }
   cp_wait<0>();
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // bulk stores complete

@@ -69,6 +69,14 @@ def main():
         print("count tables in  ", q(rel[:, 1]))
         print("count phase done ", q(rel[:, 2]))
         print("scan+publish     ", q(rel[:, 3]))
+        w0 = rel.reshape(ncta, W, SLOTS)[:, 0, :]
+        print("warp0 look-back  ", q(w0[:, 3] - w0[:, 2]), " done at", q(w0[:, 3]))
+        print("warp0 agg publish", q(w0[:, 5]), " (look-back proper", q(w0[:, 3] - w0[:, 5]), ")")
+        raw0 = t.reshape(ncta, W, SLOTS)[:, 0, :]
+        print("first poll done  ", q(w0[:, 6]), " last round ready", q(w0[:, 7]), " polls", q(raw0[:, 8] * 1000.0))
+        first_flush = rel[:, 4]
+        if (first_flush > 0).any():
+            print("first flush start", q(first_flush))
         print("decode phase done", q(rel[:, SLOTS - 2]))
         print("finish           ", q(rel[:, SLOTS - 1]))
         cta_end = rel[:, SLOTS - 1].reshape(ncta, W).max(1)
