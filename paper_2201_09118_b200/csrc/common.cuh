@@ -39,7 +39,7 @@ struct TableHdr {
 //   wlut8 uint4[256] next 8 bits -> up to 6 whole codewords for decoding plus
 //                    the count of every whole codeword for counting:
 //                    x = s0 | s1<<16, y = s2 | s3<<16, z = s4 | s5<<16,
-//                    w = bits | n<<4 | ncount<<8 | cbits<<12 | len0<<16
+//                    w = bits | n<<4 | ncount<<8 | cbits<<12 | len0<<16 | 2n<<28
 //                    (n symbols in `bits` bits; ncount whole codewords in
 //                    cbits bits; w == 0: the first code is longer than 8 bits)
 //   clut8 u8[256]    next 8 bits -> (ncode<<3) | (bits-1) over every whole

@@ -200,16 +200,16 @@ __device__ __forceinline__ uint32_t skew_addr(uint32_t base_s, uint32_t j) { ret
 struct SR {
   uint32_t w0, w1, w2;  // MSB-first words at the cursor
   uint32_t off;         // bit offset into w0 (0..31)
-  uint32_t wi;          // logical index of the word after w2
+  uint32_t wl;          // logical index of w2 (the word reloaded every step)
   uint32_t base;        // shared address of the tile buffer
   __device__ __forceinline__ void init(uint32_t base_s, uint32_t rel) {
     const uint32_t j = rel >> 5;
-    base = base_s;
+    base = pin(base_s);
     w0 = lds32(skew_addr(base_s, j));
     w1 = lds32(skew_addr(base_s, j + 1));
     w2 = lds32(skew_addr(base_s, j + 2));
     off = rel & 31;
-    wi = j + 3;
+    wl = j + 2;
   }
   __device__ __forceinline__ uint32_t peek() const { return __funnelshift_l(w1, w0, off); }
   __device__ __forceinline__ void skip(uint32_t n) {  // n <= 32
@@ -217,8 +217,8 @@ struct SR {
     const uint32_t adv = t >> 5;
     w0 = adv ? w1 : w0;
     w1 = adv ? w2 : w1;
-    wi += adv;
-    w2 = lds32(skew_addr(base, wi - 1));  // the word after w1 (unchanged when adv == 0): no branch
+    wl += adv;
+    w2 = lds32(skew_addr(base, wl));  // the word after w1 (unchanged when adv == 0): no branch
     off = t & 31;
   }
 };
@@ -344,22 +344,24 @@ __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const F
     // halfword store, then three aligned word stores (an odd start shifts the
     // entry by one halfword; the seventh halfword written is garbage inside
     // the lane's own range, overwritten by its next store)
+    int32_t k2 = 2 * k;  // remaining staging bytes
 #pragma unroll (kUnroll)
-    while (k >= 7) {
+    while (k2 >= 14) {
       const uint4 w = lds128(wl + ((r.peek() >> dsh) << dstr));
       if (!w.w) break;  // a code the table does not hold: one entry below
-      const uint32_t odd = dst & 2u;
-      const uint32_t sel = odd ? 0x5432u : 0x3210u;
-      const uint32_t a4 = (dst & ~3u) + (odd << 1);
+      const uint32_t odd = dst & 2u;                   // halfword-odd start
+      const uint32_t sel = 0x3210u + odd * 0x1111u;    // 0x5432 when odd
+      const uint32_t a4 = dst + odd;                   // first aligned word after it
       sts16(dst, w.x);
       sts32(a4, __byte_perm(w.x, w.y, sel));
       sts32(a4 + 4, __byte_perm(w.y, w.z, sel));
       sts32(a4 + 8, __byte_perm(w.z, w.z, sel));
-      const int32_t n = (int32_t)((w.w >> 4) & 15u);
-      dst += (uint32_t)n << 1;
-      k -= n;
+      const uint32_t nb = w.w >> 28;                   // 2n: bytes of staging written
+      dst += nb;
+      k2 -= (int32_t)nb;
       r.skip(w.w & 15u);
     }
+    k = k2 >> 1;
     if (k <= 0) break;
     // one entry with predicated stores: the last few symbols, or a long code
     const uint32_t win = r.peek();

@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
     wl.x = sy[0] | (sy[1] << 16);
     wl.y = sy[2] | (sy[3] << 16);
     wl.z = sy[4] | (sy[5] << 16);
-    wl.w = n6 ? (p6 | (n6 << 4) | (l0 << 16)) : 0u;
+    wl.w = n6 ? (p6 | (n6 << 4) | (l0 << 16) | ((2 * n6) << 28)) : 0u;
     wlut12[v] = wl;
   }
   uint16_t* s_len12 = reinterpret_cast<uint16_t*>(s_lut);  // 4096 lengths (8 KB)
@@ -275,7 +275,7 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
     wl.x = sy[0] | (sy[1] << 16);
     wl.y = sy[2] | (sy[3] << 16);
     wl.z = sy[4] | (sy[5] << 16);
-    wl.w = n6 ? (p6 | (n6 << 4) | (n << 8) | (pos << 12) | (l0 << 16)) : 0u;
+    wl.w = n6 ? (p6 | (n6 << 4) | (n << 8) | (pos << 12) | (l0 << 16) | ((2 * n6) << 28)) : 0u;
     reinterpret_cast<uint4*>(reinterpret_cast<char*>(blob) + L.wlut8)[v] = wl;
   }
 }
