@@ -296,22 +296,21 @@ __device__ __forceinline__ uint32_t clen(uint32_t win, const FTab& T) {
 __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, const FTab& T, uint32_t& n) {
   const uint32_t ct = pin(T.c12);
   while (pos < stop) {
-    // tight loop: whole entries that end at or before the window end
+    // tight loop: whole entries that end at or before the window end (one
+    // extra lookup when an entry ends exactly at it)
+    uint32_t y, b;
 #pragma unroll (kUnroll)
     while (true) {
-      const uint32_t y = lds16(ct + ((r.peek() >> (32 - FB)) << 1));
-      const uint32_t b = y >> 12;
+      y = lds16(ct + ((r.peek() >> (32 - FB)) << 1));
+      b = y >> 12;
       if (y == 0 || pos + b > stop) break;
       n += __popc(y & 0xfffu);
       r.skip(b);
       pos += b;
-      if (pos >= stop) break;
     }
     if (pos >= stop) break;
-    const uint32_t win = r.peek();
-    const uint32_t y = lds16(ct + ((win >> (32 - FB)) << 1));
     if (!y) {  // first code longer than 12 bits
-      const uint32_t l = (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
+      const uint32_t l = (fslow(r.peek(), T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
       if (!l) return false;
       n += 1;
       r.skip(l);
@@ -319,7 +318,6 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
       continue;
     }
     // the window ends inside this entry (stop - pos < b <= 12)
-    const uint32_t b = y >> 12;
     const uint32_t rem = stop - pos;
     const uint32_t mask = y & 0xfffu;
     n += __popc(mask & ((1u << rem) - 1u));
