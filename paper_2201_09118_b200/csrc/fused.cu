@@ -715,7 +715,8 @@ template <int VAR>
 __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, uint64_t tile, uint32_t base_s,
                                             uint64_t wb0, uint32_t nsl, uint32_t ep, uint32_t& e, uint32_t& c,
                                             bool& bad, int32_t seed_o = -1, uint32_t* cand_out = nullptr,
-                                            bool* fullfix = nullptr, const uint32_t* gpre = nullptr) {
+                                            bool* fullfix = nullptr, const uint32_t* gpre = nullptr,
+                                            unsigned long long* desc_out = nullptr) {
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t sb = a.sb;
   const uint64_t j0 = tile * a.sps;
@@ -803,7 +804,9 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
     if (seed_o < 0) {
       // speculative: publish the exit when it does not depend on the seed
       if (cand_out) *cand_out = cand_c;
-      if (lane == 0) st_relaxed(a.exit_desc + tile, mkdesc(ep, indep ? D_INC : D_AGG, indep ? wb0 + xlast : 0));
+      const unsigned long long dsc = mkdesc(ep, indep ? D_INC : D_AGG, indep ? wb0 + xlast : 0);
+      if (lane == 0) st_relaxed(a.exit_desc + tile, dsc);
+      if (desc_out) *desc_out = dsc;
 #ifdef BH_X_DEPSTAT
       if (lane == 0 && !indep) atomicAdd(&a.rep->pad[3], 1ull);
       if (lane == 0 && tile > 0) atomicAdd(&a.rep->pad[3], 1ull << 32);
@@ -834,7 +837,9 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
         }
       }
       const uint32_t xl = __shfl_sync(0xffffffffu, x, nsl - 1);
-      if (lane == 0) st_relaxed(a.exit_desc + tile, mkdesc(ep, D_INC, wb0 + xl));
+      const unsigned long long dsc = mkdesc(ep, D_INC, wb0 + xl);
+      if (lane == 0) st_relaxed(a.exit_desc + tile, dsc);
+      if (desc_out) *desc_out = dsc;
     }
   }
   if (!active) c = 0;
@@ -948,6 +953,11 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   __shared__ uint32_t s_wsum[32];
   __shared__ uint32_t s_carry;
   __shared__ uint32_t s_tcnt[MAX_SMEM_TILES];  // symbols per tile of the range (short ranges)
+  // SYNC, short ranges: the range's exit descriptors and full-fix flags, so
+  // the seam fix-up reads in-range predecessors from shared memory
+  constexpr uint32_t SX = VAR == BH_VARIANT_SYNC ? MAX_SMEM_TILES : 1;
+  __shared__ unsigned long long s_texit[SX];
+  __shared__ uint8_t s_tff[SX];
   const uint32_t ep = *(volatile const unsigned int*)a.ws_hdr + 1u;
   const TableHdr* hdr = static_cast<const TableHdr*>(a.table);
   if (VAR == BH_VARIANT_SYNC && !hdr->complete) {
@@ -1012,11 +1022,18 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   T.t = table_view(a.table, a.max_codes, hdr->ncodes);
   T.kind = hdr->kind;
   T.max_len = hdr->max_len ? min(hdr->max_len, 32u) : 32u;
+  if (VAR == BH_VARIANT_SYNC)
+    for (uint32_t i = threadIdx.x; i < SX; i += blockDim.x) { s_texit[i] = 0; s_tff[i] = 0; }
   __syncthreads();  // barriers initialised
   mbar_wait(bar_ct, 0);
   MARK(1);
 
   // ---- phase 1: count ----------------------------------------------------
+  // SYNC: first-slot candidate counts of this warp's tiles in its (still
+  // unused) staging buffer when they fit, else in the workspace
+  const uint32_t ktiles = t0 + wib < t1 ? (uint32_t)((t1 - (t0 + wib) + W - 1) / W) : 0u;
+  const bool scand = VAR == BH_VARIANT_SYNC && nt <= MAX_SMEM_TILES && 64 * ktiles <= 2 * a.cap;
+  uint32_t kidx = 0;
   // GAP: the gap bytes of a tile are loaded one tile ahead, like its words
   auto gap_load = [&](uint64_t t, uint32_t* g) {
     const uint64_t j = t * a.sps + lane;
@@ -1039,14 +1056,23 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
     uint32_t e, c, cand = 0;
     bool fullfix = false;
+    unsigned long long dsc = 0;
     tile_counts<VAR>(a, T, tile, dbuf_s, wb_a, nsl, ep, e, c, bad, -1, &cand, &fullfix,
-                     VAR == BH_VARIANT_GAP && a.sps == 32 ? gcur : nullptr);
+                     VAR == BH_VARIANT_GAP && a.sps == 32 ? gcur : nullptr, &dsc);
     gcur[0] = gnext[0];
     gcur[1] = gnext[1];
     if (VAR == BH_VARIANT_SYNC) {
-      a.cand[tile * 32 + lane] = (uint16_t)min(cand, 0xffffu);
-      if (lane == 0) a.tile_dlt[tile] = fullfix ? FULL_FIX : 0;
+      if (scand) sts16(stg_s + 64 * kidx + 2 * lane, min(cand, 0xffffu));
+      else a.cand[tile * 32 + lane] = (uint16_t)min(cand, 0xffffu);
+      if (lane == 0) {
+        a.tile_dlt[tile] = fullfix ? FULL_FIX : 0;
+        if (nt <= MAX_SMEM_TILES) {
+          s_tff[tile - t0] = fullfix ? 1 : 0;
+          *(volatile unsigned long long*)&s_texit[tile - t0] = dsc;
+        }
+      }
     }
+    ++kidx;
     uint32_t incl = c;
     for (int off = 1; off < 32; off <<= 1) {
       const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
@@ -1064,6 +1090,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     nch_a = nch_b;
   }
   cp_wait<0>();
+  MARK(9);
   if (VAR == BH_VARIANT_SYNC) {
     // Seam fix-up (inter_sync, sync_decoder.py:116-149).  Every exit that does
     // not depend on the seed was published during the count loop, so the
@@ -1080,15 +1107,24 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       if (!__any_sync(0xffffffffu, mine)) break;
       bool serial = false;
       if (mine && tk > 0) {
-        unsigned long long dp, ds = ld_relaxed(a.exit_desc + tk);
-        const bool ff = a.tile_dlt[tk] == FULL_FIX;
-        while (!desc_ready(dp = ld_relaxed(a.exit_desc + tk - 1), ep)) __nanosleep(32);
+        const bool sm_own = nt <= MAX_SMEM_TILES, sm_pred = sm_own && tk - 1 >= t0;
+        unsigned long long dp;
+        const unsigned long long ds = sm_own ? *(volatile unsigned long long*)&s_texit[tk - t0]
+                                             : ld_relaxed(a.exit_desc + tk);
+        const bool ff = sm_own ? s_tff[tk - t0] != 0 : a.tile_dlt[tk] == FULL_FIX;
+        if (sm_pred) {
+          while (!desc_ready(dp = *(volatile unsigned long long*)&s_texit[tk - 1 - t0], ep)) __nanosleep(32);
+        } else {
+          while (!desc_ready(dp = ld_relaxed(a.exit_desc + tk - 1), ep)) __nanosleep(32);
+        }
         if ((ds & D_INC) && (dp & D_INC) && !ff) {
           const uint32_t o = (uint32_t)((dp & D_VAL) - tk * a.seq_bits);
           if (o >= 32) {
             bad = true;
           } else if (o) {
-            const int32_t dl = (int32_t)a.cand[tk * 32 + o] - (int32_t)a.cand[tk * 32];
+            const uint32_t cs = stg_s + 64 * (uint32_t)(kb + lane);
+            const int32_t dl = scand ? (int32_t)lds16(cs + 2 * o) - (int32_t)lds16(cs)
+                                     : (int32_t)a.cand[tk * 32 + o] - (int32_t)a.cand[tk * 32];
             a.tile_dlt[tk] = dl;
             a.lane_info[tk * 32] = o;  // first slot enters at the seed; prefix 0
             if (nt <= MAX_SMEM_TILES) s_tcnt[tk - t0] += (uint32_t)dl;
@@ -1107,18 +1143,29 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         const uint32_t j = __ffs(sm_mask) - 1;
         sm_mask &= sm_mask - 1;
         const uint64_t st = t0 + wib + (kb + j) * W;
+        const bool sm_own = nt <= MAX_SMEM_TILES, sm_pred = sm_own && st - 1 >= t0;
         unsigned long long dp = 0;
-        if (lane == 0)
-          while (!((dp = ld_relaxed(a.exit_desc + st - 1)) & D_INC) || !desc_ready(dp, ep)) __nanosleep(32);
+        if (lane == 0) {
+          if (sm_pred) {
+            while (!((dp = *(volatile unsigned long long*)&s_texit[st - 1 - t0]) & D_INC) || !desc_ready(dp, ep))
+              __nanosleep(32);
+          } else {
+            while (!((dp = ld_relaxed(a.exit_desc + st - 1)) & D_INC) || !desc_ready(dp, ep)) __nanosleep(32);
+          }
+        }
         dp = __shfl_sync(0xffffffffu, dp, 0);
         const uint32_t o = (uint32_t)((dp & D_VAL) - st * a.seq_bits);
-        const unsigned long long ds = ld_relaxed(a.exit_desc + st);
-        const bool ff = __shfl_sync(0xffffffffu, lane == 0 ? (uint32_t)(a.tile_dlt[st] == FULL_FIX) : 0u, 0) != 0;
+        const unsigned long long ds = sm_own ? *(volatile unsigned long long*)&s_texit[st - t0]
+                                             : ld_relaxed(a.exit_desc + st);
+        const bool ff = sm_own ? s_tff[st - t0] != 0
+                               : __shfl_sync(0xffffffffu, lane == 0 ? (uint32_t)(a.tile_dlt[st] == FULL_FIX) : 0u, 0) != 0;
         if ((ds & D_INC) && !ff) {  // first-slot swap behind a dependent predecessor
           if (o >= 32) {
             bad = true;
           } else if (lane == 0) {
-            const int32_t dl = (int32_t)a.cand[st * 32 + o] - (int32_t)a.cand[st * 32];
+            const uint32_t cs = stg_s + 64 * (uint32_t)(kb + j);
+            const int32_t dl = scand ? (int32_t)lds16(cs + 2 * o) - (int32_t)lds16(cs)
+                                     : (int32_t)a.cand[st * 32 + o] - (int32_t)a.cand[st * 32];
             a.tile_dlt[st] = dl;
             a.lane_info[st * 32] = o;
             if (nt <= MAX_SMEM_TILES) s_tcnt[st - t0] += (uint32_t)dl;
@@ -1137,7 +1184,10 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         __syncwarp();
         const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - st * a.sps);
         uint32_t e, c;
-        tile_counts<VAR>(a, T, st, dbuf_s, wbs, nsl, ep, e, c, bad, (int32_t)min(o, 255u));
+        unsigned long long dsc = 0;
+        tile_counts<VAR>(a, T, st, dbuf_s, wbs, nsl, ep, e, c, bad, (int32_t)min(o, 255u), nullptr, nullptr,
+                         nullptr, &dsc);
+        if (lane == 0 && nt <= MAX_SMEM_TILES) *(volatile unsigned long long*)&s_texit[st - t0] = dsc;
         uint32_t incl = c;
         for (int off = 1; off < 32; off <<= 1) {
           const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);

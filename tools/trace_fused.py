@@ -67,6 +67,7 @@ def main():
     if os.environ.get("BH_FUSED_V", "2") != "1":
         print("start            ", q(rel[:, 0]))
         print("count tables in  ", q(rel[:, 1]))
+        print("count loop done  ", q(rel[:, 9]))
         print("count phase done ", q(rel[:, 2]))
         print("scan+publish     ", q(rel[:, 3]))
         w0 = rel.reshape(ncta, W, SLOTS)[:, 0, :]
