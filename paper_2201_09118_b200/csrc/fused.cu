@@ -437,7 +437,9 @@ __device__ __forceinline__ bool resync_step(uint32_t base_s, uint32_t eo, uint32
 
 __device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co, uint32_t xo, uint32_t en,
                                        uint32_t stop, const FTab& T, uint32_t& cn, uint32_t& xn) {
-  if (T.dsh != 24) return resync_step(base_s, eo, co, xo, en, stop, T, cn, xn);  // wide layout
+  // long-code books (wide layout): a 12-bit entry holds a codeword or two, so
+  // the plain per-codeword walk is cheaper there
+  if (T.dsh != 24) return resync_step(base_s, eo, co, xo, en, stop, T, cn, xn);
   uint32_t po = eo, pn = en, no = 0, nn = 0;
   SR ro, rn;
   ro.init(base_s, po);
@@ -446,39 +448,67 @@ __device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co
   while (true) {
     if (pn >= stop) { cn = nn; xn = pn; return true; }
     if (po == pn) { cn = nn + (co - no); xn = xo; return true; }
-    const bool old_low = po < pn;
-    SR& r = old_low ? ro : rn;
-    const uint32_t win = r.peek();
-    const uint32_t y = lds16(ct + ((win >> (32 - FB)) << 1));
-    if (!y) {  // a code longer than 12 bits: one codeword
-      const uint32_t l = (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
-      if (!l) return false;
-      r.skip(l);
-      if (old_low) { po += l; ++no; } else { pn += l; ++nn; }
-      continue;
+    if (po < pn) {  // the old parse is behind: advance it a whole entry
+      const uint32_t win = ro.peek();
+      const uint32_t y = lds16(ct + ((win >> (32 - FB)) << 1));
+      if (!y) {  // a code longer than 12 bits: one codeword
+        const uint32_t l = (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
+        if (!l) return false;
+        ro.skip(l);
+        po += l;
+        ++no;
+        continue;
+      }
+      const uint32_t mask = y & 0xfffu, b = y >> 12, d = pn - po;
+      uint32_t adv;
+      if (d < b) {
+        if ((mask >> d) & 1u) {  // the old parse has a start where the new one is: they meet
+          no += __popc(mask & ((1u << d) - 1u));
+          po = pn;
+          continue;
+        }
+        const uint32_t hi = mask >> d;  // step over it to the first start after it
+        adv = hi ? d + __ffs(hi) - 1 : b;
+        no += __popc(mask & ((1u << adv) - 1u));
+      } else {
+        adv = b;
+        no += __popc(mask);
+      }
+      ro.skip(adv);
+      po += adv;
+    } else {  // the new parse is behind: advance it, never past the window end
+      const uint32_t win = rn.peek();
+      const uint32_t y = lds16(ct + ((win >> (32 - FB)) << 1));
+      if (!y) {
+        const uint32_t l = (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
+        if (!l) return false;
+        rn.skip(l);
+        pn += l;
+        ++nn;
+        continue;
+      }
+      const uint32_t mask = y & 0xfffu, b = y >> 12, d = po - pn, rem = stop - pn;
+      uint32_t adv;
+      if (d < b && ((mask >> d) & 1u) && d < rem) {  // meet before the window end
+        nn += __popc(mask & ((1u << d) - 1u));
+        pn = po;
+        continue;
+      }
+      if (rem < b) {  // the window ends inside this entry
+        nn += __popc(mask & ((1u << rem) - 1u));
+        const uint32_t hi = mask >> rem;
+        adv = hi ? rem + __ffs(hi) - 1 : b;
+      } else if (d < b) {
+        const uint32_t hi = mask >> d;
+        adv = hi ? d + __ffs(hi) - 1 : b;
+        nn += __popc(mask & ((1u << adv) - 1u));
+      } else {
+        adv = b;
+        nn += __popc(mask);
+      }
+      rn.skip(adv);
+      pn += adv;
     }
-    const uint32_t mask = y & 0xfffu, b = y >> 12;
-    const uint32_t lo = old_low ? po : pn, d = old_low ? pn - po : po - pn;  // d >= 1
-    const uint32_t rem = old_low ? 0xffffu : stop - pn;                     // new parse: room to stop
-    uint32_t adv, cnt;
-    if (d < b && ((mask >> d) & 1u) && d < rem) {  // the lower parse has a start where the other is
-      adv = d;
-      cnt = __popc(mask & ((1u << d) - 1u));
-    } else if (rem < b) {  // new parse: the window ends inside this entry
-      cnt = __popc(mask & ((1u << rem) - 1u));
-      const uint32_t hi = mask >> rem;
-      adv = hi ? rem + __ffs(hi) - 1 : b;
-    } else if (d < b) {  // steps over the other cursor: stop at the first start after it
-      const uint32_t hi = mask >> d;
-      adv = hi ? d + __ffs(hi) - 1 : b;
-      cnt = __popc(mask & ((1u << adv) - 1u));
-    } else {
-      adv = b;
-      cnt = __popc(mask);
-    }
-    (void)lo;
-    r.skip(adv);
-    if (old_low) { po += adv; no += cnt; } else { pn += adv; nn += cnt; }
   }
 }
 
