@@ -179,13 +179,6 @@ __device__ __forceinline__ uint32_t pin(uint32_t v) {
   return v;
 }
 
-// predicated shared load (no branch): returns `v` unchanged when !p
-__device__ __forceinline__ uint32_t lds32_if(uint32_t a, uint32_t p, uint32_t v) {
-  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.b32 q, %2, 0;\n\t@q ld.shared.u32 %0, [%1];\n\t}"
-               : "+r"(v) : "r"(a), "r"(p) : "memory");
-  return v;
-}
-
 // Bit reader over a tile's staged words (tile-relative bit positions): the
 // current and next word plus one prefetched word, and a bit offset.  peek is
 // one funnel shift; skip advances by at most one word with selects and a
@@ -269,12 +262,6 @@ __device__ __forceinline__ uint32_t fone(uint32_t win, const FTab& T) {
   const uint4 w = lds128(T.wl + ((win >> T.dsh) << T.dst));
   if (w.w) return (w.x & 0xffffu) | (((w.w >> 16) & 15u) << 16);
   return flong(win, T);
-}
-
-__device__ __forceinline__ uint32_t flen(uint32_t win, const FTab& T) {
-  const uint32_t y = lds128(T.wl + ((win >> T.dsh) << T.dst)).w;
-  if (y) return (y >> 16) & 15u;
-  return (flong(win, T) >> 16) & 0xffu;
 }
 
 // length of one codeword from the 12-bit count table (second start, or the end
@@ -516,12 +503,6 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
 }
-__device__ __forceinline__ void cp_async16_ca(uint32_t s, const void* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async8_ca(uint32_t s, const void* gmem) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(s), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
@@ -632,37 +613,8 @@ __device__ __forceinline__ void flush_compact(uint16_t* __restrict__ out, uint64
   }
 }
 
-// Flush [P, P+C) from staging aligned to the output: stg symbol i <-> output
-// (P & ~7) + i.  Whole chunks: one aligned 128-bit shared load and one
-// 128-bit global store; the edge chunks shared with neighbouring tiles go
-// element by element.
-__device__ __forceinline__ void flush_aligned_stg(uint16_t* __restrict__ out, uint64_t nsym, uint64_t P, uint32_t C,
-                                                  uint32_t stg_s) {
-  const uint32_t lane = threadIdx.x & 31;
-  const uint64_t a0 = P & ~7ull, g1 = P + C;
-  const uint64_t f0 = (P + 7) & ~7ull;                   // first whole chunk
-  const uint64_t f1 = (g1 < nsym ? g1 : nsym) & ~7ull;   // end of whole chunks
-  if (f1 > f0) {
-    const uint32_t c0 = (uint32_t)(f0 - a0) >> 3;
-    const uint32_t nfull = (uint32_t)((f1 - f0) >> 3);
-    for (uint32_t ch = lane; ch < nfull; ch += 32) {
-      const uint4 v = lds128(stg_s + 16 * (c0 + ch));
-      *reinterpret_cast<uint4*>(out + f0 + 8ull * ch) = v;
-    }
-  }
-  const uint64_t hend = f0 < g1 ? f0 : g1;
-  const uint64_t tbeg = f1 > hend ? f1 : hend;
-  const uint32_t nh = (uint32_t)(hend - P), nt = (uint32_t)(g1 - tbeg);
-  if (lane < nh) {
-    const uint64_t g = P + lane;
-    if (g < nsym) out[g] = (uint16_t)lds16(stg_s + 2 * (uint32_t)(g - a0));
-  } else if (lane >= 8 && lane - 8 < nt) {
-    const uint64_t g = tbeg + (lane - 8);
-    if (g < nsym) out[g] = (uint16_t)lds16(stg_s + 2 * (uint32_t)(g - a0));
-  }
-}
-
-// Same as flush_aligned_stg, but the whole 16-byte chunks leave shared memory
+// Flush [P, P+C) from staging aligned to the output (stg symbol i <-> output
+// (P & ~7) + i): the whole 16-byte chunks leave shared memory
 // as ONE bulk (TMA) copy issued by lane 0 -- no registers or load/store
 // instructions per chunk.  The staging must not be rewritten before the copy
 // has read it (bulk_read_wait).  Returns whether a copy was issued.
@@ -805,9 +757,11 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
     if (tile > 0) {
       // the true seed lies within the codeword straddling the boundary, so
       // only offsets below the longest code length are candidates
+#ifndef BH_X_NOCAND
       if (lane < T.max_len) {
         if (!resync(base_s, b0, c0, x0, b0 + lane, stop0, T, cand_c, cand_x)) cand_x = 0xffffffffu;
       }
+#endif
       indep = __all_sync(0xffffffffu, cand_x == x0);
     }
     const uint32_t xlast = __shfl_sync(0xffffffffu, x, nsl - 1);
