@@ -1365,7 +1365,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     nch_a = nch_b;
   }
   cp_wait<0>();
-  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // bulk stores complete
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging read (writes land by kernel end)
   if (!have_off) mbar_wait(bar_off, 0);  // keep warp 0's arrival inside the CTA's lifetime
   if (__any_sync(0xffffffffu, bad) && lane == 0) tag_status(a.rep, ep, BH_INVALID);
   MARK(TRACE_SLOTS - 2);
