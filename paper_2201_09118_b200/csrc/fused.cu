@@ -936,6 +936,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   __shared__ unsigned long long s_ctaoff;
   __shared__ uint32_t s_wsum[32];
   __shared__ uint32_t s_carry;
+  __shared__ uint32_t s_next;  // phase 2: next tile of the range to take
   __shared__ uint32_t s_tcnt[MAX_SMEM_TILES];  // symbols per tile of the range (short ranges)
   // SYNC, short ranges: the range's exit descriptors and full-fix flags, so
   // the seam fix-up reads in-range predecessors from shared memory
@@ -1008,6 +1009,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   T.max_len = hdr->max_len ? min(hdr->max_len, 32u) : 32u;
   if (VAR == BH_VARIANT_SYNC)
     for (uint32_t i = threadIdx.x; i < SX; i += blockDim.x) { s_texit[i] = 0; s_tff[i] = 0; }
+  if (threadIdx.x == 0) s_next = W;  // phase 2 starts with tile t0 + warp index
   __syncthreads();  // barriers initialised
   mbar_wait(bar_ct, 0);
   MARK(1);
@@ -1260,13 +1262,20 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   MARK(3);
 
   // ---- phase 2: decode and write -----------------------------------------
+  // tiles are taken dynamically (a shared counter): a warp that finishes
+  // early takes the next tile, so the range's last round is balanced
   tile = t0 + wib;
   if (tile < t1) wb_a = stage_words(a, tile, land, nch_a);
   cp_commit();
   bool have_off = false, bulk_pending = false;
   unsigned long long Pc = 0;
-  for (; tile < t1; tile += W) {
-    const uint64_t tn = tile + W;
+  auto grab = [&]() -> uint64_t {
+    uint32_t v = 0;
+    if (lane == 0) v = atomicAdd(&s_next, 1u);
+    return t0 + __shfl_sync(0xffffffffu, v, 0);
+  };
+  for (; tile < t1;) {
+    const uint64_t tn = grab();
     const uint32_t info = a.lane_info[tile * 32 + lane];
     uint32_t C, toff;
     if (nt <= MAX_SMEM_TILES) {
@@ -1363,6 +1372,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     __syncwarp();
     wb_a = wb_b;
     nch_a = nch_b;
+    tile = tn;
   }
   cp_wait<0>();
   if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging read (writes land by kernel end)
