@@ -1274,9 +1274,22 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     if (lane == 0) v = atomicAdd(&s_next, 1u);
     return t0 + __shfl_sync(0xffffffffu, v, 0);
   };
+  // the tile's lane info (entry, prefix) and seam delta are loaded one tile
+  // ahead, like its words
+  uint32_t info_n = 0;
+  int32_t dlt_n = 0;
+  if (tile < t1) {
+    info_n = a.lane_info[tile * 32 + lane];
+    if (VAR == BH_VARIANT_SYNC) dlt_n = a.tile_dlt[tile];
+  }
   for (; tile < t1;) {
     const uint64_t tn = grab();
-    const uint32_t info = a.lane_info[tile * 32 + lane];
+    const uint32_t info = info_n;
+    const int32_t dlt = dlt_n;
+    if (tn < t1) {
+      info_n = a.lane_info[tn * 32 + lane];
+      if (VAR == BH_VARIANT_SYNC) dlt_n = a.tile_dlt[tn];
+    }
     uint32_t C, toff;
     if (nt <= MAX_SMEM_TILES) {
       const uint32_t ti = (uint32_t)(tile - t0);
@@ -1299,7 +1312,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     const uint32_t b = (uint32_t)((tile * a.sps + lane) * a.sb - wb_a);
     const uint32_t e = b + (info & 0xffffu);
     uint32_t o = info >> 16;
-    if (VAR == BH_VARIANT_SYNC && lane > 0) o += (uint32_t)a.tile_dlt[tile];  // seam fix of slot 0
+    if (VAR == BH_VARIANT_SYNC && lane > 0) o += (uint32_t)dlt;  // seam fix of slot 0
     const uint32_t on = __shfl_down_sync(0xffffffffu, o, 1);
     const uint32_t c = lane < nsl ? (lane == 31 ? C : on) - o : 0u;
     if (!have_off) {
