@@ -337,11 +337,13 @@ __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const F
       const uint32_t odd = dst & 2u;                   // halfword-odd start
       const uint32_t sel = 0x3210u + odd * 0x1111u;    // 0x5432 when odd
       const uint32_t a4 = dst + odd;                   // first aligned word after it
+      const uint32_t nb = w.w >> 28;                   // 2n: bytes of staging written
       sts16(dst, w.x);
       sts32(a4, __byte_perm(w.x, w.y, sel));
-      sts32(a4 + 4, __byte_perm(w.y, w.z, sel));
-      sts32(a4 + 8, __byte_perm(w.z, w.z, sel));
-      const uint32_t nb = w.w >> 28;                   // 2n: bytes of staging written
+      // the last two words only when the entry reaches them (fewer, less
+      // conflicted shared-memory wavefronts)
+      if (nb > 4 + odd) sts32(a4 + 4, __byte_perm(w.y, w.z, sel));  // symbol 2 (3 if odd) present
+      if (nb > 8 + odd) sts32(a4 + 8, __byte_perm(w.z, w.z, sel));  // symbol 4 (5 if odd) present
       dst += nb;
       k2 -= (int32_t)nb;
       r.skip(w.w & 15u);
