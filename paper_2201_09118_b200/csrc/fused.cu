@@ -338,7 +338,7 @@ __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const F
       const uint32_t sel = 0x3210u + odd * 0x1111u;    // 0x5432 when odd
       const uint32_t a4 = dst + odd;                   // first aligned word after it
       const uint32_t nb = w.w >> 28;                   // 2n: bytes of staging written
-      sts16(dst, w.x);
+      if (odd) sts16(dst, w.x);  // an even start is covered by the first word
       sts32(a4, __byte_perm(w.x, w.y, sel));
       // the last two words only when the entry reaches them (fewer, less
       // conflicted shared-memory wavefronts)
