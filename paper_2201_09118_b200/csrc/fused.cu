@@ -1,8 +1,8 @@
 // fused.cu -- the fused decoders: the bh_decode fast path (one kernel per decode).
 //
 // k_fused2 runs one persistent CTA per SM; CTA c owns a contiguous range of
-// tiles (a tile = one sequence = `subseqs_per_seq` subsequences, one lane per
-// subsequence).  Two phases:
+// tiles (a tile = 32 subsequences -- one sequence at the reference's default
+// layout -- one lane per subsequence, whatever the stream's subseqs_per_seq).  Two phases:
 //
 //   phase 1 (count): each warp takes tiles of the range round-robin, stages
 //     the tile's words with cp.async (double buffer) and computes every
@@ -1408,7 +1408,13 @@ using namespace bh;
 
 namespace {
 inline uint64_t nsub_of(const bh_stream* s) { return (s->total_bits + s->subseq_bits - 1) / s->subseq_bits; }
-inline uint64_t nseq_of(const bh_stream* s) { return (nsub_of(s) + s->subseqs_per_seq - 1) / s->subseqs_per_seq; }
+// The fused kernel's tile is 32 subsequences (one lane each) whatever the
+// stream's subseqs_per_seq: the decoded symbols do not depend on how
+// subsequences are grouped into sequences (the synchronised state is the
+// unique fixpoint -- entry i is the first codeword start at or after boundary
+// i), so every layout runs with full warps.
+constexpr uint32_t TILE_SUBSEQ = 32;
+inline uint64_t nseq_of(const bh_stream* s) { return (nsub_of(s) + TILE_SUBSEQ - 1) / TILE_SUBSEQ; }
 
 int env_int(const char* name, int dflt) {
   const char* v = getenv(name);
@@ -1421,7 +1427,7 @@ struct FusedCfg {
 
 FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   FusedCfg c;
-  const uint32_t seq_bits = s->subseq_bits * s->subseqs_per_seq;
+  const uint32_t seq_bits = s->subseq_bits * TILE_SUBSEQ;
   // words one tile can stage: its span (+1 for a straddle), the 16-byte
   // alignment of the first word (+3), the halo, rounded up to 16 bytes
   c.wpb = ((seq_bits + 31) / 32 + 1 + 3 + HALO_WORDS + 3) & ~3u;
@@ -1432,7 +1438,7 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   const double per_bit = s->total_bits ? (double)s->symbol_count / (double)s->total_bits : 1.0;
   uint32_t cap = (uint32_t)(seq_bits * per_bit * BH_CAPF) + BH_CAPADD;
   if (env_int("BH_FUSED_CAP", 0)) cap = (uint32_t)env_int("BH_FUSED_CAP", 0);
-  const uint32_t cmax = s->subseqs_per_seq * (s->subseq_bits + 31) + 16;
+  const uint32_t cmax = TILE_SUBSEQ * (s->subseq_bits + 31) + 16;
   if (cap > cmax) cap = cmax;
   if (cap < 64) cap = 64;
   c.cap = (cap + 7) & ~7u;
@@ -1507,8 +1513,8 @@ extern "C" int bh_debug_fused_shape(const bh_stream* s, const bh_tune* tune, uin
 extern "C" int bh_fused_supported(const bh_stream* s, int variant) {
   if (env_int("BH_DISABLE_FUSED", 0)) return 0;
   if (variant != BH_VARIANT_GAP && variant != BH_VARIANT_SYNC) return 0;
-  if (s->subseqs_per_seq > 32 || s->subseqs_per_seq == 0) return 0;
-  const uint64_t seq_bits = (uint64_t)s->subseq_bits * s->subseqs_per_seq;
+  if (s->subseqs_per_seq == 0) return 0;
+  const uint64_t seq_bits = (uint64_t)s->subseq_bits * TILE_SUBSEQ;
   if (seq_bits > 16384 || s->total_bits >= (1ull << 36) || s->symbol_count >= (1ull << 36)) return 0;
   if (variant == BH_VARIANT_GAP && !s->gap_dev) return 0;
   FusedCfg c = fused_cfg(s);
@@ -1540,8 +1546,8 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.table = s->table_dev;
   a.max_codes = s->max_codes;
   a.sb = s->subseq_bits;
-  a.sps = s->subseqs_per_seq;
-  a.seq_bits = s->subseq_bits * s->subseqs_per_seq;
+  a.sps = TILE_SUBSEQ;
+  a.seq_bits = s->subseq_bits * TILE_SUBSEQ;
   a.tb = s->total_bits;
   a.nsym = s->symbol_count;
   a.nsub = nsub_of(s);
