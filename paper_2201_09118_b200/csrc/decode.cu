@@ -593,6 +593,7 @@ extern "C" int bh_report_read(const void* report_dev, bh_report* out, void* cuda
     const uint32_t ep = (uint32_t)r.pad[1];
     const unsigned long long tag = r.pad[0];
     out->status = (uint32_t)(tag >> 32) == ep ? (int32_t)(0x7fffffffu - (uint32_t)tag) : BH_OK;
+    if (ep && (uint32_t)r.pad[3] == ep) out->status = BH_NEED_STAGED;  // fused path declined
   }
   out->fail_slot = r.fail_slot;
   out->bits_sync = r.bits_sync;

@@ -60,7 +60,6 @@ constexpr int kUnroll = BH_UNR;  // unroll of the tight count/decode loops
 #endif
 constexpr int FUSED_MAX_WARPS = BH_MAXW;
 constexpr int FUSED_MAX_THREADS = 32 * FUSED_MAX_WARPS;  // 24 warps: up to 85 registers per thread
-constexpr uint32_t NEED_STAGED = 9;  // BH_NEED_STAGED
 
 // descriptor: [63:38] epoch (26 bits) | [37:36] flags | [35:0] value
 constexpr unsigned long long D_VAL = (1ull << 36) - 1;
@@ -100,6 +99,8 @@ struct FusedArgs {
   uint32_t tables_bytes;
   uint32_t has_l12;      // 12-bit second-level table staged (codes longer than 8 bits)
   uint32_t first_entry;  // bh_stream.first_entry
+  uint32_t spl;          // stream subsequences per lane ("virtual" subsequence = spl real ones)
+  uint64_t nsub_r;       // real subsequences (gap array length)
   uint32_t wide;         // table layout: 1 = wlut12, 0 = replicated wlut8 (+ lut12 if has_l12)
   uint32_t t_lim, t_c12, t_wp, t_l12;  // shared-memory table offsets (bytes)
   uint32_t t_ljs, ljs_bytes;            // shared copy of ljsym for the limit search (0 bytes: global)
@@ -120,6 +121,12 @@ constexpr unsigned long long FUSED_MARK = 0xF05EDull;  // rep->pad[2]: report wr
 constexpr uint32_t T_LIMBASE = 2 * 33 * 8;  // lim u64[33], base i64[33] (contiguous)
 constexpr uint32_t T_NARROW_DEC = 256 * 8 * 16;
 constexpr uint32_t T_WIDE_DEC = 16 * FB_SIZE;
+
+// rep->pad[3] = epoch: the fused path declined this call (overrides every
+// status; bh_decode reruns the reference-structured pipeline)
+__device__ __forceinline__ void flag_need_staged(DevReport* rep, uint32_t ep) {
+  *(volatile unsigned long long*)&rep->pad[3] = ep;
+}
 
 __device__ __forceinline__ void tag_status(DevReport* rep, uint32_t ep, uint32_t status) {
   unsigned long long v = ((unsigned long long)ep << 32) | (unsigned long long)(0x7fffffffu - status);
@@ -669,23 +676,6 @@ __device__ __forceinline__ void flush_aligned(uint16_t* __restrict__ out, uint64
   }
 }
 
-// GAP: tile-relative entry and stop of this lane's slot (gap_decoder.py:24-53)
-__device__ __forceinline__ void gap_window(const FusedArgs& a, uint64_t tile, uint64_t wb0, uint32_t nsl,
-                                           uint32_t& e, uint32_t& stop) {
-  const uint32_t lane = threadIdx.x & 31;
-  const bool active = lane < nsl;
-  const uint64_t j = tile * a.sps + lane;
-  const uint32_t b = (uint32_t)(j * a.sb - wb0);
-  const uint32_t tbr = (uint32_t)min(a.tb - wb0, (uint64_t)0xffffffffu);
-  const uint32_t g = active ? a.gap[j] : 0u;
-  uint32_t gn = __shfl_down_sync(0xffffffffu, g, 1);
-  if (lane == nsl - 1) gn = (j + 1 < a.nsub) ? a.gap[j + 1] : 0u;
-  e = b + g;
-  stop = (j + 1 < a.nsub) ? b + a.sb + gn : tbr;
-  if (stop > tbr) stop = tbr;
-  if (!active) stop = e;
-}
-
 // Entries and counts of one tile (lane = subsequence); positions are relative
 // to the tile buffer's first bit `wb0`.  GAP: boundary + gap byte; SYNC:
 // intra-sequence chain rounds plus the seam seed from the predecessor tile's
@@ -701,6 +691,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
                                             bool& bad, int32_t seed_o = -1, uint32_t* cand_out = nullptr,
                                             bool* fullfix = nullptr, const uint32_t* gpre = nullptr,
                                             unsigned long long* desc_out = nullptr) {
+  bool resync_needed = false;  // GAP, spl > 1: an inner gap entry is not a codeword start
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t sb = a.sb;
   const uint64_t j0 = tile * a.sps;
@@ -713,9 +704,10 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
   c = 0;
   if (VAR == BH_VARIANT_GAP) {
     // gpre: this lane's gap byte and lane 31's successor, prefetched by the caller
-    const uint32_t g = gpre ? gpre[0] : (active ? a.gap[j] : 0u);
+    // virtual subsequence j starts at real subsequence j * spl (its gap byte)
+    const uint32_t g = gpre ? gpre[0] : (active ? a.gap[j * a.spl] : 0u);
     uint32_t gn = __shfl_down_sync(0xffffffffu, g, 1);
-    if (lane == nsl - 1) gn = gpre && nsl == 32 ? gpre[1] : ((j + 1 < a.nsub) ? a.gap[j + 1] : 0u);
+    if (lane == nsl - 1) gn = gpre && nsl == 32 ? gpre[1] : ((j + 1 < a.nsub) ? a.gap[(j + 1) * a.spl] : 0u);
     e = b + g;
     stop = (j + 1 < a.nsub) ? b + sb + gn : tbr;
     if (stop > tbr) stop = tbr;
@@ -723,6 +715,20 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
     if (active && e < stop) {
       SR r;
       r.init(base_s, e);
+      // a lane spanning spl stream subsequences checks that every inner gap
+      // entry is one of its codeword starts (then the reference's windows
+      // hold exactly the same codewords); a corrupt inner entry sends the
+      // decode to the reference-structured pipeline, which reproduces the
+      // reference's error
+      const uint32_t sbr = sb / a.spl;
+      for (uint32_t k = 1; k < a.spl; ++k) {
+        const uint64_t jr = j * a.spl + k;
+        if (jr >= a.nsub_r) break;
+        const uint32_t ek = b + k * sbr + a.gap[jr];
+        if (ek < x || ek > stop) { resync_needed = true; break; }
+        if (!fcount(r, x, ek, T, c)) bad = true;
+        if (x != ek) { resync_needed = true; break; }
+      }
       if (!fcount(r, x, stop, T, c)) bad = true;
     }
   } else {
@@ -793,10 +799,6 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
       const unsigned long long dsc = mkdesc(ep, indep ? D_INC : D_AGG, indep ? wb0 + xlast : 0);
       if (lane == 0) st_relaxed(a.exit_desc + tile, dsc);
       if (desc_out) *desc_out = dsc;
-#ifdef BH_X_DEPSTAT
-      if (lane == 0 && !indep) atomicAdd(&a.rep->pad[3], 1ull);
-      if (lane == 0 && tile > 0) atomicAdd(&a.rep->pad[3], 1ull << 32);
-#endif
     } else if (tile > 0) {
       const uint32_t o = (uint32_t)seed_o;
       const uint32_t sc = __shfl_sync(0xffffffffu, cand_c, o & 31);
@@ -829,6 +831,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
     }
   }
   if (!active) c = 0;
+  if (VAR == BH_VARIANT_GAP && resync_needed) flag_need_staged(a.rep, ep);
 }
 
 // Completion: the last CTA of the call records the epoch in the report and
@@ -948,7 +951,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   const uint32_t ep = *(volatile const unsigned int*)a.ws_hdr + 1u;
   const TableHdr* hdr = static_cast<const TableHdr*>(a.table);
   if (VAR == BH_VARIANT_SYNC && !hdr->complete) {
-    if (blockIdx.x == 0 && threadIdx.x == 0) tag_status(a.rep, ep, NEED_STAGED);
+    if (blockIdx.x == 0 && threadIdx.x == 0) flag_need_staged(a.rep, ep);
     fused_finish(a, ep);
     return;
   }
@@ -1025,8 +1028,8 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   // GAP: the gap bytes of a tile are loaded one tile ahead, like its words
   auto gap_load = [&](uint64_t t, uint32_t* g) {
     const uint64_t j = t * a.sps + lane;
-    g[0] = (lane < a.sps && j < a.nsub) ? a.gap[j] : 0u;
-    g[1] = (lane == 31 && t * a.sps + 32 < a.nsub) ? a.gap[t * a.sps + 32] : 0u;
+    g[0] = (lane < a.sps && j < a.nsub) ? a.gap[j * a.spl] : 0u;
+    g[1] = (lane == 31 && t * a.sps + 32 < a.nsub) ? a.gap[(t * a.sps + 32) * a.spl] : 0u;
   };
   uint32_t gcur[2] = {0, 0}, gnext[2] = {0, 0};
   if (VAR == BH_VARIANT_GAP && tile < t1) gap_load(tile, gcur);
@@ -1407,6 +1410,11 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
 using namespace bh;
 
 namespace {
+int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
+}
+
 inline uint64_t nsub_of(const bh_stream* s) { return (s->total_bits + s->subseq_bits - 1) / s->subseq_bits; }
 // The fused kernel's tile is 32 subsequences (one lane each) whatever the
 // stream's subseqs_per_seq: the decoded symbols do not depend on how
@@ -1414,12 +1422,24 @@ inline uint64_t nsub_of(const bh_stream* s) { return (s->total_bits + s->subseq_
 // unique fixpoint -- entry i is the first codeword start at or after boundary
 // i), so every layout runs with full warps.
 constexpr uint32_t TILE_SUBSEQ = 32;
-inline uint64_t nseq_of(const bh_stream* s) { return (nsub_of(s) + TILE_SUBSEQ - 1) / TILE_SUBSEQ; }
-
-int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  return v && *v ? atoi(v) : dflt;
+// Low-CR streams decode faster with longer lane windows: a lane takes spl
+// consecutive stream subsequences (a "virtual" subsequence of spl * subseq_bits
+// bits, entered at the first one's gap byte -- again the same fixpoint), as
+// long as a tile's output stays within ~4 KB of staging.
+inline uint32_t spl_of(const bh_stream* s) {
+  const int e = env_int("BH_FUSED_SPL", 0);
+  if (e == 1 || e == 2 || e == 4) return (uint32_t)e;
+  const double per_bit = s->total_bits ? (double)s->symbol_count / (double)s->total_bits : 1.0;
+  uint32_t spl = 1;
+  while (spl < 4 && 32.0 * 2 * spl * s->subseq_bits * per_bit <= 2048.0 && 32ull * 2 * spl * s->subseq_bits <= 16384)
+    spl *= 2;
+  return spl;
 }
+inline uint32_t vsb_of(const bh_stream* s) { return s->subseq_bits * spl_of(s); }
+inline uint64_t vnsub_of(const bh_stream* s) { return (s->total_bits + vsb_of(s) - 1) / vsb_of(s); }
+inline uint64_t nseq_of(const bh_stream* s) { return (vnsub_of(s) + TILE_SUBSEQ - 1) / TILE_SUBSEQ; }
+
+
 
 struct FusedCfg {
   uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12, wide, t_lim, t_c12, t_wp, t_l12, t_ljs, ljs_bytes;
@@ -1427,7 +1447,7 @@ struct FusedCfg {
 
 FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   FusedCfg c;
-  const uint32_t seq_bits = s->subseq_bits * TILE_SUBSEQ;
+  const uint32_t seq_bits = vsb_of(s) * TILE_SUBSEQ;
   // words one tile can stage: its span (+1 for a straddle), the 16-byte
   // alignment of the first word (+3), the halo, rounded up to 16 bytes
   c.wpb = ((seq_bits + 31) / 32 + 1 + 3 + HALO_WORDS + 3) & ~3u;
@@ -1438,7 +1458,7 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   const double per_bit = s->total_bits ? (double)s->symbol_count / (double)s->total_bits : 1.0;
   uint32_t cap = (uint32_t)(seq_bits * per_bit * BH_CAPF) + BH_CAPADD;
   if (env_int("BH_FUSED_CAP", 0)) cap = (uint32_t)env_int("BH_FUSED_CAP", 0);
-  const uint32_t cmax = TILE_SUBSEQ * (s->subseq_bits + 31) + 16;
+  const uint32_t cmax = TILE_SUBSEQ * (vsb_of(s) + 31) + 16;
   if (cap > cmax) cap = cmax;
   if (cap < 64) cap = 64;
   c.cap = (cap + 7) & ~7u;
@@ -1467,13 +1487,13 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   c.tables += c.ljs_bytes;
   // two word buffers, staging
   c.per_warp = (uint32_t)align16(8 * (size_t)c.wpb + 2 * (size_t)c.cap + 32);
+  // dynamic shared memory budget: 227 KB per CTA minus the kernel's static
+  // arrays (tile totals, seam descriptors: < 8 KB)
+  const int fit = (int)(((int64_t)(219 * 1024) - (int64_t)c.tables) / (int64_t)c.per_warp);
   int w = env_int("BH_FUSED_WARPS", 0);
-  if (w <= 0) {
-    w = (int)((223 * 1024 - c.tables) / c.per_warp);
-    if (w > FUSED_MAX_WARPS) w = FUSED_MAX_WARPS;
-    if (w < 1) w = 1;
-  }
+  if (w <= 0 || w > fit) w = fit;
   if (w > FUSED_MAX_WARPS) w = FUSED_MAX_WARPS;
+  if (w < 1) w = 1;
   // small inputs: fewer warps per CTA so that every SM gets a group
   static int sms = 0;
   if (!sms) {
@@ -1514,11 +1534,11 @@ extern "C" int bh_fused_supported(const bh_stream* s, int variant) {
   if (env_int("BH_DISABLE_FUSED", 0)) return 0;
   if (variant != BH_VARIANT_GAP && variant != BH_VARIANT_SYNC) return 0;
   if (s->subseqs_per_seq == 0) return 0;
-  const uint64_t seq_bits = (uint64_t)s->subseq_bits * TILE_SUBSEQ;
+  const uint64_t seq_bits = (uint64_t)vsb_of(s) * TILE_SUBSEQ;
   if (seq_bits > 16384 || s->total_bits >= (1ull << 36) || s->symbol_count >= (1ull << 36)) return 0;
   if (variant == BH_VARIANT_GAP && !s->gap_dev) return 0;
   FusedCfg c = fused_cfg(s);
-  return c.smem <= 227 * 1024 ? 1 : 0;
+  return c.smem <= 219 * 1024 ? 1 : 0;
 }
 
 // workspace: [64 B header: epoch, CTA-done counter][cnt desc][exit desc]
@@ -1545,12 +1565,14 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.gap = s->gap_dev;
   a.table = s->table_dev;
   a.max_codes = s->max_codes;
-  a.sb = s->subseq_bits;
+  a.sb = vsb_of(s);
   a.sps = TILE_SUBSEQ;
-  a.seq_bits = s->subseq_bits * TILE_SUBSEQ;
+  a.spl = spl_of(s);
+  a.seq_bits = vsb_of(s) * TILE_SUBSEQ;
   a.tb = s->total_bits;
   a.nsym = s->symbol_count;
-  a.nsub = nsub_of(s);
+  a.nsub = vnsub_of(s);
+  a.nsub_r = nsub_of(s);
   a.nseq = nseq;
   a.out = out_dev;
   a.ws_hdr = static_cast<unsigned int*>(ws);
