@@ -30,7 +30,8 @@ extern "C" {
 #define BH_GAPOVERFLOW 6   /* GapOverflow (encoder.py:86-87) */
 #define BH_BAD_ARGUMENT 7  /* ValueError-class misuse (layout, capacity < 1, ...) */
 #define BH_CUDA_ERROR 8    /* CUDA runtime failure */
-#define BH_NEED_STAGED 9   /* fused path declined (incomplete codebook); bh_decode reruns staged */
+#define BH_NEED_STAGED 9   /* fused path declined (incomplete codebook, or a gap entry inside a
+                                  lane window that is not a codeword start); bh_decode reruns staged */
 
 #define BH_VARIANT_GAP 1     /* gap_decoder.decode (gap_decoder.py:71-92) */
 #define BH_VARIANT_SYNC 2    /* sync_decoder.decode (sync_decoder.py:173-211) */
