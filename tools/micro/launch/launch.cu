@@ -1,4 +1,5 @@
 // Fixed cost of launching a persistent kernel, measured like bench.py (events
+// build: nvcc -O2 -gencode arch=compute_100a,code=sm_100a -o tools/micro/launch/launch tools/micro/launch/launch.cu
 // around the launch, a 256 MiB memset between steps so the host runs ahead).
 #include <cstdio>
 #include <cuda_runtime.h>
