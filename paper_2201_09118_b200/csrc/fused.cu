@@ -1081,6 +1081,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     nch_a = nch_b;
   }
   cp_wait<0>();
+  __syncwarp();  // candidate slots written by other lanes are read below
   MARK(9);
   if (VAR == BH_VARIANT_SYNC) {
     // Seam fix-up (inter_sync, sync_decoder.py:116-149).  Every exit that does
