@@ -1016,6 +1016,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     for (uint32_t i = threadIdx.x; i < SX; i += blockDim.x) { s_texit[i] = 0; s_tff[i] = 0; }
   if (threadIdx.x == 0) s_next = W;  // phase 2 starts with tile t0 + warp index
   __syncthreads();  // barriers initialised
+  MARK(56);
   mbar_wait(bar_ct, 0);
   MARK(1);
 
@@ -1039,6 +1040,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     __syncwarp();
     skew_in(land_s, dbuf_s, nch_a);
     __syncwarp();
+    if (kidx < 8) MARK(10 + 2 * kidx);
     if (tn < t1) {  // the next tile's words land while this one is counted
       wb_b = stage_words(a, tn, land, nch_b);
       if (VAR == BH_VARIANT_GAP) gap_load(tn, gnext);
@@ -1050,6 +1052,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     unsigned long long dsc = 0;
     tile_counts<VAR>(a, T, tile, dbuf_s, wb_a, nsl, ep, e, c, bad, -1, &cand, &fullfix,
                      VAR == BH_VARIANT_GAP && a.sps == 32 ? gcur : nullptr, &dsc);
+    if (kidx < 8) MARK(11 + 2 * kidx);
     gcur[0] = gnext[0];
     gcur[1] = gnext[1];
     if (VAR == BH_VARIANT_SYNC) {
@@ -1288,6 +1291,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     info_n = a.lane_info[tile * 32 + lane];
     if (VAR == BH_VARIANT_SYNC) dlt_n = a.tile_dlt[tile];
   }
+  uint32_t dk = 0;  // tiles decoded (trace slots)
   for (; tile < t1;) {
     const uint64_t tn = grab();
     const uint32_t info = info_n;
@@ -1309,6 +1313,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     }
     cp_wait<0>();  // this tile's words have landed
     __syncwarp();
+    if (dk < 8) MARK(30 + 3 * dk);
     skew_in(land_s, dbuf_s, nch_a);
     __syncwarp();
     if (tn < t1) wb_b = stage_words(a, tn, land, nch_b);  // lands while this tile decodes
@@ -1338,6 +1343,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       if (!fdecode(r, c, stg_s + 2 * (sh + o), T)) bad = true;
     }
     __syncwarp();
+    if (dk < 8) MARK(31 + 3 * dk);
 
     const bool aligned = have_off;
     if (!have_off) {
@@ -1389,6 +1395,8 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       }
     }
     __syncwarp();
+    if (dk < 8) MARK(32 + 3 * dk);
+    ++dk;
     wb_a = wb_b;
     nch_a = nch_b;
     tile = tn;
