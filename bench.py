@@ -220,8 +220,14 @@ def count_launches(fn) -> int:
 
 
 def e2e_measure(stream, book, variant: str, steps: int, flush):
-    """Public C-ABI call with pinned host buffers: H2D of payload+gap+lengths,
-    table build, decode, D2H of the decoded symbols -- all inside the events."""
+    """Public C-ABI calls with pinned host buffers: H2D of payload+gap+lengths,
+    table build, decode, D2H of the decoded symbols, every step inside the
+    timed region.  Two calls are in flight, each with its own device buffers,
+    workspace, report and CUDA stream (the ABI is stream-ordered with no
+    hidden synchronisation), so one call's H2D and decode overlap the
+    previous call's D2H on the other copy engine.  Each step starts with an
+    L2 flush on its stream (inside the timed region).  Returns the whole
+    region's time per step (ms), the last output, and the bytes moved."""
     import torch
     from paper_2201_09118_b200 import _lib
     from paper_2201_09118_b200._lib import check, stream_handle
@@ -234,38 +240,62 @@ def e2e_measure(stream, book, variant: str, steps: int, flush):
     gap_h = torch.from_numpy(stream.gap.copy()).pin_memory()
     lens = book.length_bytes()
     lens_h = torch.from_numpy(lens.copy()).pin_memory()
-    out_h = torch.empty(stream.symbol_count, dtype=torch.int16).pin_memory()
-    words = torch.zeros(nwords + _lib.WORD_PAD, dtype=torch.int32, device=dev)
-    gap_d = torch.empty(len(stream.gap), dtype=torch.uint8, device=dev)
-    lens_d = torch.empty(len(lens), dtype=torch.uint8, device=dev)
     max_codes = len(book.entries)
-    table = torch.empty(lib.bh_table_bytes(max_codes), dtype=torch.uint8, device=dev)
-    out_d = empty(stream.symbol_count, np.uint16, dev)
     lay = stream.layout
-    cs = _lib.Stream(words.data_ptr(), stream.total_bits, stream.symbol_count, lay.subseq_bits,
-                     lay.subseqs_per_seq, 16, max_codes, gap_d.data_ptr(), table.data_ptr())
     var = _lib.VARIANT_GAP if variant == "gap" else _lib.VARIANT_SYNC
     tune = make_tune(max_len=stream.codebook.max_len)
-    wsb = lib.bh_workspace_bytes(C.byref(cs), var, C.byref(tune))
-    ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)
-    lib.bh_workspace_reset(ws.data_ptr(), ws.numel(), stream_handle())
-    rep = DeviceReport(dev).init()
 
-    def step():
-        st = stream_handle()
-        words[:nwords].copy_(units_h, non_blocking=True)
-        gap_d.copy_(gap_h, non_blocking=True)
-        lens_d.copy_(lens_h, non_blocking=True)
-        check(lib.bh_table_build(lens_d.data_ptr(), len(lens), table.data_ptr(), max_codes, st), "table")
-        check(lib.bh_decode_async(C.byref(cs), var, C.byref(tune), out_d.data_ptr(), ws.data_ptr(), wsb,
-                                  rep.ptr, st), "decode")
-        out_h.copy_(out_d[: stream.symbol_count], non_blocking=True)
+    class Ctx:
+        def __init__(self):
+            self.st = torch.cuda.Stream(device=dev)
+            self.out_h = torch.empty(stream.symbol_count, dtype=torch.int16).pin_memory()
+            self.words = torch.zeros(nwords + _lib.WORD_PAD, dtype=torch.int32, device=dev)
+            self.gap_d = torch.empty(len(stream.gap), dtype=torch.uint8, device=dev)
+            self.lens_d = torch.empty(len(lens), dtype=torch.uint8, device=dev)
+            self.table = torch.empty(lib.bh_table_bytes(max_codes), dtype=torch.uint8, device=dev)
+            self.out_d = empty(stream.symbol_count, np.uint16, dev)
+            self.cs = _lib.Stream(self.words.data_ptr(), stream.total_bits, stream.symbol_count,
+                                  lay.subseq_bits, lay.subseqs_per_seq, 16, max_codes,
+                                  self.gap_d.data_ptr(), self.table.data_ptr())
+            self.wsb = lib.bh_workspace_bytes(C.byref(self.cs), var, C.byref(tune))
+            self.ws = torch.empty(max(self.wsb, 256), dtype=torch.uint8, device=dev)
+            lib.bh_workspace_reset(self.ws.data_ptr(), self.ws.numel(), stream_handle(self.st))
+            self.rep = DeviceReport(dev).init()
 
-    times = time_steps(step, steps, 2, flush)
-    r = rep.read()
-    check(r.status, "e2e decode")
-    got = out_h.numpy().view(np.uint16)
-    return times, got, 4 * nwords + len(stream.gap) + len(lens), 2 * stream.symbol_count
+        def step(self):
+            with torch.cuda.stream(self.st):
+                st = stream_handle(self.st)
+                flush()
+                self.words[:nwords].copy_(units_h, non_blocking=True)
+                self.gap_d.copy_(gap_h, non_blocking=True)
+                self.lens_d.copy_(lens_h, non_blocking=True)
+                check(lib.bh_table_build(self.lens_d.data_ptr(), len(lens), self.table.data_ptr(), max_codes, st),
+                      "table")
+                check(lib.bh_decode_async(C.byref(self.cs), var, C.byref(tune), self.out_d.data_ptr(),
+                                          self.ws.data_ptr(), self.wsb, self.rep.ptr, st), "decode")
+                self.out_h.copy_(self.out_d[: stream.symbol_count], non_blocking=True)
+
+    ctx = [Ctx(), Ctx()]
+    torch.cuda.synchronize()
+    for i in range(4):  # warm-up
+        ctx[i % 2].step()
+    torch.cuda.synchronize()
+    main = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(main)
+    for c in ctx:
+        c.st.wait_event(a)
+    for i in range(steps):
+        ctx[i % 2].step()
+    for c in ctx:
+        main.wait_stream(c.st)
+    b.record(main)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    for c in ctx:
+        check(c.rep.read().status, "e2e decode")
+    got = ctx[(steps - 1) % 2].out_h.numpy().view(np.uint16)
+    return ms, got, 4 * nwords + len(stream.gap) + len(lens), 2 * stream.symbol_count
 
 
 # --------------------------------------------------------------------------
@@ -629,10 +659,11 @@ def main():
     if not args.no_extras:
         # e2e through the public C-ABI call with host buffers
         ksteps = max(3, min(args.steps, 50))
-        et, got, bi, bo = e2e_measure(stream, book, args.variant, ksteps, flush)
+        ems, got, bi, bo = e2e_measure(stream, book, args.variant, ksteps, flush)
         assert np.array_equal(got, codes), "e2e decode mismatch"
-        line["e2e"] = {"value": 2 * n * ksteps / (sum(et) / 1e3) / 1e9, "unit": "GB/s",
-                       "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "steps": ksteps}
+        line["e2e"] = {"value": 2 * n / (ems / 1e3) / 1e9, "unit": "GB/s",
+                       "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "steps": ksteps,
+                       "ms_per_step": ems, "in_flight": 2}
         # other variants and the in-run coarse-grained cuSZ-style baseline
         variants = {args.variant: value / world}
         other = "sync" if args.variant == "gap" else "gap"
