@@ -72,7 +72,7 @@ def main():
         d[f"b{bi}_lens"] = lens
         d[f"b{bi}_meta"] = np.array([st.total_bits, st.symbol_count, lay.unit_bits, lay.units_per_subseq,
                                      lay.subseqs_per_seq], np.int64)
-        for k in range(14):
+        for k in range(60):
             kind = KINDS[k % len(KINDS)]
             units, gap = st.units.copy(), st.gap.copy()
             tb, cnt = st.total_bits, st.symbol_count
@@ -92,9 +92,14 @@ def main():
             elif kind == "count":
                 b = int(rng.choice([-7, -1, 1, 5]))
                 cnt = max(0, cnt + b)
-            else:
+            else:  # a stream cut short: drop the tail units, zero the bits past the new end
                 b = int(rng.integers(1, 40))
                 tb = tb - b
+                ub = lay.unit_bits
+                units = units[: -(-tb // ub)].copy()
+                if tb % ub:
+                    units[-1] &= np.uint32(((1 << ub) - 1) ^ ((1 << (ub - tb % ub)) - 1))
+                gap = gap[: -(-tb // (lay.unit_bits * lay.units_per_subseq))].copy()
             try:
                 bad = ph.EncodedStream(layout=lay, units=units, total_bits=tb, symbol_count=cnt,
                                        codebook=book, gap=gap)

@@ -50,6 +50,10 @@ def damaged(ph, i):
         cnt = max(0, cnt + b)
     else:
         tb -= b
+        units = units[: -(-tb // ub)].copy()
+        if tb % ub:
+            units[-1] &= np.uint32(((1 << ub) - 1) ^ ((1 << (ub - tb % ub)) - 1))
+        gap = gap[: -(-tb // (ub * ups))].copy()
     return ph.EncodedStream(layout=ph.LayoutConfig(ub, ups, sps), units=units, total_bits=tb, symbol_count=cnt,
                             codebook=book, gap=gap)
 
