@@ -5,11 +5,26 @@
 // this), zero padded by >= BH_WORD_PAD words so 64-bit windows never fault and
 // reads past the payload return zero bits exactly like kernels.py:30-31.
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 #include "../../include/b200huff.h"
 
 namespace bh {
+
+// SM count of the calling thread's current device, cached per device
+// (thread-safe; 148 if the query fails)
+inline int device_sm_count() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+  int n = cache[dev].load(std::memory_order_relaxed);
+  if (n <= 0) {
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev].store(n, std::memory_order_relaxed);
+  }
+  return n;
+}
 
 constexpr int LUT_BITS = 11;                 // first-level window (2^11 entries)
 constexpr int LUT_SIZE = 1 << LUT_BITS;

@@ -562,16 +562,7 @@ inline bool bad_stream(const bh_stream* s) {
   return !s || s->subseq_bits == 0 || s->subseqs_per_seq == 0 || (s->total_bits && !s->words_dev) ||
          !s->table_dev;
 }
-int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+int sm_count() { return device_sm_count(); }
 }  // namespace
 
 extern "C" int bh_device_sm_count(void) { return sm_count(); }

@@ -1504,13 +1504,7 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   if (w > FUSED_MAX_WARPS) w = FUSED_MAX_WARPS;
   if (w < 1) w = 1;
   // small inputs: fewer warps per CTA so that every SM gets a group
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
+  const int sms = device_sm_count();
   const uint64_t nseq = nseq_of(s);
   if (!env_int("BH_FUSED_WARPS", 0) && nseq < (uint64_t)sms * (uint64_t)w) {
     w = (int)((nseq + sms - 1) / sms);
@@ -1523,7 +1517,7 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
 
 }  // namespace
 
-static unsigned long long* g_trace = nullptr;
+static std::atomic<unsigned long long*> g_trace{nullptr};  // debug only
 
 // Debug: record a per-warp timeline of the next fused launches into trace_dev
 // (u64[grid * warps * 64] globaltimer stamps); NULL switches it off.
@@ -1607,16 +1601,11 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.t_l12 = cfg.t_l12;
   a.t_ljs = cfg.t_ljs;
   a.ljs_bytes = cfg.ljs_bytes;
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
-  a.trace = g_trace;
+  const int sms = device_sm_count();
+  a.trace = g_trace.load(std::memory_order_relaxed);
   const void* fn =
-      variant == BH_VARIANT_GAP ? (g_trace ? (const void*)k_fused2<BH_VARIANT_GAP, 1> : (const void*)k_fused2<BH_VARIANT_GAP, 0>)
-                                : (g_trace ? (const void*)k_fused2<BH_VARIANT_SYNC, 1> : (const void*)k_fused2<BH_VARIANT_SYNC, 0>);
+      variant == BH_VARIANT_GAP ? (a.trace ? (const void*)k_fused2<BH_VARIANT_GAP, 1> : (const void*)k_fused2<BH_VARIANT_GAP, 0>)
+                                : (a.trace ? (const void*)k_fused2<BH_VARIANT_SYNC, 1> : (const void*)k_fused2<BH_VARIANT_SYNC, 0>);
   // launch attributes and occupancy cached per (kernel, threads, smem)
   static std::mutex mu;
   static std::map<std::tuple<const void*, uint32_t, uint32_t>, int> occ;
