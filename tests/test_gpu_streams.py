@@ -59,3 +59,54 @@ def test_two_streams_in_flight(ph, variant):
     for c in ctxs:
         check(c["rep"].read().status, "decode")
         assert np.array_equal(c["host"].numpy().view(np.uint16), c["codes"])
+
+
+def test_host_threads_decode_concurrently(ph):
+    """Four host threads, each with its own stream/workspace/report, call the
+    library at the same time (ctypes drops the GIL inside the calls); the
+    launch-configuration caches are shared and must stay consistent."""
+    import threading
+
+    import torch
+    from paper_2201_09118_b200 import _lib
+    from paper_2201_09118_b200._lib import check, stream_handle
+    from paper_2201_09118_b200._pipeline import make_tune
+    from paper_2201_09118_b200.device import DeviceReport, device_stream, empty
+    from paper_2201_09118_b200.synth import gaussian_codes
+    lib = _lib.load()
+    fields = []
+    for k, sigma in enumerate((0.6, 3.0, 8.0, 22.0)):
+        codes = gaussian_codes(600_000, 1024, sigma, seed=40 + k)
+        st = ph.encode(codes, ph.book_for(codes, 16), ph.DEFAULT_LAYOUT, with_gap=True)
+        fields.append((codes, st, device_stream(st)))
+    torch.cuda.synchronize()
+    errors = []
+
+    def worker(k):
+        try:
+            codes, st, ds = fields[k]
+            var = _lib.VARIANT_GAP if k % 2 == 0 else _lib.VARIANT_SYNC
+            tune = make_tune(max_len=st.codebook.max_len)
+            cs = torch.cuda.Stream()
+            wsb = lib.bh_workspace_bytes(C.byref(ds.c), var, C.byref(tune))
+            ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=ds.device)
+            out = empty(len(codes), np.uint16, ds.device)
+            with torch.cuda.stream(cs):
+                lib.bh_workspace_reset(ws.data_ptr(), ws.numel(), stream_handle(cs))
+                rep = DeviceReport(ds.device).init()
+                for _ in range(5):
+                    check(lib.bh_decode_async(C.byref(ds.c), var, C.byref(tune), out.data_ptr(), ws.data_ptr(),
+                                              wsb, rep.ptr, stream_handle(cs)), "decode")
+            cs.synchronize()
+            check(rep.read().status, "decode")
+            if not np.array_equal(out.cpu().numpy().view(np.uint16), codes):
+                errors.append((k, "mismatch"))
+        except Exception as e:  # noqa: BLE001 -- reported below
+            errors.append((k, repr(e)))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert errors == []
