@@ -495,7 +495,7 @@ def run_multifield(args, rank, world):
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()
-    with ClockSampler(int(os.environ.get("LOCAL_RANK", 0))) as clk:
+    with ClockSampler(torch.cuda.current_device()) as clk:
         if world > 1:
             torch.distributed.barrier()
         times = time_steps(fn, args.steps, args.warmup, lambda: flush_buf.zero_())
@@ -549,10 +549,18 @@ def main():
         return run_reference(args)
     rank, local, world = dist_env()
     import torch
+    # BH_BENCH_SHARED_DEVICE=1 (testing the N-rank code path on a one-GPU
+    # box): every rank on cuda:0, gloo for the barriers and reductions
+    shared = os.environ.get("BH_BENCH_SHARED_DEVICE") == "1"
+    if shared:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     if args.config == "multifield":
         return run_multifield(args, rank, world)
     import paper_2201_09118_b200 as ph
@@ -659,10 +667,16 @@ def main():
     if not args.no_extras:
         # e2e through the public C-ABI call with host buffers
         ksteps = max(3, min(args.steps, 50))
+        if world > 1:
+            torch.distributed.barrier()
         ems, got, bi, bo = e2e_measure(stream, book, args.variant, ksteps, flush)
         assert np.array_equal(got, codes), "e2e decode mismatch"
-        line["e2e"] = {"value": 2 * n / (ems / 1e3) / 1e9, "unit": "GB/s",
-                       "h2d_bytes_per_step": bi, "d2h_bytes_per_step": bo, "steps": ksteps,
+        if world > 1:  # whole job: every rank's field, slowest rank's time
+            te = torch.tensor([ems], dtype=torch.float64, device="cuda")
+            torch.distributed.all_reduce(te, op=torch.distributed.ReduceOp.MAX)
+            ems = float(te.item())
+        line["e2e"] = {"value": world * 2 * n / (ems / 1e3) / 1e9, "unit": "GB/s",
+                       "h2d_bytes_per_step": world * bi, "d2h_bytes_per_step": world * bo, "steps": ksteps,
                        "ms_per_step": ems, "in_flight": 2}
         # other variants and the in-run coarse-grained cuSZ-style baseline
         variants = {args.variant: value / world}
