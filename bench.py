@@ -226,9 +226,9 @@ def e2e_measure(stream, book, variant: str, steps: int, flush):
     workspace, report and CUDA stream (the ABI is stream-ordered with no
     hidden synchronisation), so one call's H2D and decode overlap the
     previous call's D2H on the other copy engine.  Each step starts with an
-    L2 flush on its stream (inside the timed region).  Returns the whole
-    median region's time per step (ms) over three regions, the last output,
-    the bytes moved and the three per-region times."""
+    L2 flush on its stream (inside the timed region).  Returns the time per
+    step (ms) of the median of three timed regions, the last output, the
+    bytes moved and the three per-region times."""
     import torch
     from paper_2201_09118_b200 import _lib
     from paper_2201_09118_b200._lib import check, stream_handle
