@@ -70,6 +70,8 @@ typedef struct bh_tune {
     uint32_t max_len;            /* longest code length when known (0 = unknown); <= 8 lets the
                                     fused kernel leave the 12-bit second-level table out of
                                     shared memory (more warps per SM) */
+    uint32_t ctas;               /* fused kernel CTAs (0 = one per SM): several decodes on
+                                    concurrent streams can share the GPU in one wave */
 } bh_tune;
 
 /* Decode report, mirroring DecodeStats (staging.py:31-45) plus status. */
@@ -88,6 +90,18 @@ typedef struct bh_report {
     uint64_t seam_passes;
     uint64_t repair_needed;
     uint64_t pad[4];
+    /* Device phase boundaries (globaltimer ns) of the last call, valid when the
+     * report was initialised (bh_report_init; bh_decode always does): [0] start,
+     * then the end of each phase in the reference's order --
+     *   GAP  (gap_decoder.py:82-92):  [1] entries_from_gap, [3] count_pass
+     *                                 (incl. the output index), [4] tune,
+     *                                 [5] decode_write;  [2] count loop end
+     *   SYNC (sync_decoder.py:185-211): [1] intra_sync, [2] inter_sync,
+     *                                 [3] output_index, [4] tune, [5] decode_write
+     * The fused kernel stamps them in-kernel (max over CTAs; tune takes no
+     * time there), the staged pipeline with a one-thread stamp kernel between
+     * its launches. */
+    uint64_t phase_ns[6];
 } bh_report;
 
 /* ---- library ---------------------------------------------------------- */

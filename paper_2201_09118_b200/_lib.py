@@ -40,7 +40,7 @@ class Tune(C.Structure):
     _fields_ = [
         ("t_high", U32), ("capacity", U32), ("capacity_table", U32 * 64),
         ("early_exit", U32), ("collect_stats", U32), ("fused", U32), ("seam_passes", U32),
-        ("max_len", U32),
+        ("max_len", U32), ("ctas", U32),
     ]
 
 
@@ -50,7 +50,7 @@ class Report(C.Structure):
         ("bits_sync", U64), ("bits_count", U64), ("bits_write", U64),
         ("write_rounds", U64), ("staged_slots", U64), ("bypass_slots", U64),
         ("total_symbols", U64), ("stale_seams", U64), ("seam_passes", U64),
-        ("repair_needed", U64), ("pad", U64 * 4),
+        ("repair_needed", U64), ("pad", U64 * 4), ("phase_ns", U64 * 6),
     ]
 
 

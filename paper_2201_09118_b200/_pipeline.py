@@ -9,12 +9,13 @@ single-pass kernels.
 from __future__ import annotations
 
 import ctypes as C
+import time
 
 import numpy as np
 
 from . import _lib
 from ._lib import check, load, ptr, require_cuda, stream_handle
-from ._timing import add
+from ._timing import split_phases
 from .device import Workspace, d2h, device_stream, empty
 from .staging import DEFAULT_CAPACITY
 
@@ -42,6 +43,7 @@ def make_tune(capacity: int = DEFAULT_CAPACITY, tuner_config=None, collect_stats
 
 def run_decode(stream, variant: int, capacity: int = DEFAULT_CAPACITY, tuner_config=None,
                stats=None, timings=None, return_device: bool = False, fused: bool | None = None):
+    t_enter = time.perf_counter()
     torch = require_cuda()
     lib = load()
     ds = device_stream(stream)
@@ -53,22 +55,23 @@ def run_decode(stream, variant: int, capacity: int = DEFAULT_CAPACITY, tuner_con
     wsb = lib.bh_decode_workspace_bytes(ds.ref, variant, C.byref(tune))
     ws = Workspace.get(wsb, ds.device)
     rep = _lib.Report()
-    t0 = torch.cuda.Event(enable_timing=True)
-    t1 = torch.cuda.Event(enable_timing=True)
-    t0.record()
+    if timings is not None:
+        torch.cuda.current_stream(ds.device).synchronize()  # uploads belong to the first phase
+    t_call = time.perf_counter()
     status = lib.bh_decode(ds.ref, variant, C.byref(tune), ptr(out), ptr(ws), wsb, C.byref(rep),
                            stream_handle())
-    t1.record()
     check(status, "decode", rep.fail_slot)
-    if timings is not None:
-        t1.synchronize()
-        add(timings, "decode", t0.elapsed_time(t1) / 1e3)
     if stats is not None:
         if variant == _lib.VARIANT_SYNC:
             stats.add_bits("sync", rep.bits_sync)
         else:
             stats.add_bits("count_pass", rep.bits_count)
         stats.absorb_write(rep)
-    if return_device:
-        return out[:n] if n else out[:0]
-    return d2h(out, np.uint16)[:n]
+    res = (out[:n] if n else out[:0]) if return_device else d2h(out, np.uint16)[:n]
+    if timings is not None:
+        if return_device:
+            torch.cuda.current_stream(ds.device).synchronize()
+        t_end = time.perf_counter()
+        split_phases(timings, variant == _lib.VARIANT_GAP, list(rep.phase_ns), t_call - t_enter,
+                     t_end - t_call, tuner_config is not None)
+    return res

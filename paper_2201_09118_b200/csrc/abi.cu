@@ -194,16 +194,20 @@ static int staged_pipeline(const bh_stream* s, int variant, const bh_tune* tune,
   const int stats = tune && tune->collect_stats;
   int rc;
   prof_mark(S(st), "start");
+  stamp_phase(rep, 0, S(st));
   if (variant == BH_VARIANT_GAP) {
     if ((rc = bh_entries_from_gap(s, entries, st))) return rc;
     prof_mark(S(st), "entries_from_gap");
+    stamp_phase(rep, 1, S(st));
     if ((rc = bh_count_windows(s, 1, entries, counts, exits, rep, st))) return rc;
     prof_mark(S(st), "count_pass");
+    stamp_phase(rep, 2, S(st));
   } else {
     if ((rc = bh_intra_sync_ex(s, nullptr, 0, nullptr, entries, exits, counts, at<uint8_t>(ws, L.synced),
                                at<int32_t>(ws, L.iters), at<void>(ws, L.flags), 2 * ns + 8 * nq + 16, rep, st)))
       return rc;
     prof_mark(S(st), "intra_sync");
+    stamp_phase(rep, 1, S(st));
     unsigned long long* ctr = at<unsigned long long>(ws, L.seam_ctr);
     int64_t* seeds = at<int64_t>(ws, L.seeds);
     if (nq > 1) {
@@ -241,10 +245,12 @@ static int staged_pipeline(const bh_stream* s, int variant, const bh_tune* tune,
       }
     }
     prof_mark(S(st), "inter_sync");
+    stamp_phase(rep, 2, S(st));
   }
   if ((rc = bh_output_index(counts, ns, oi, at<void>(ws, L.scan), bh_scan_workspace_bytes(ns), st))) return rc;
   if ((rc = bh_check_total(s, oi, variant == BH_VARIANT_GAP ? BH_BADGAP : BH_TRUNCATED, rep, st))) return rc;
   prof_mark(S(st), "output_index");
+  stamp_phase(rep, 3, S(st));
   if (tune && tune->t_high) {
     const uint32_t C = tune->t_high + 1;
     int64_t* seqc = at<int64_t>(ws, L.seqc);
@@ -262,16 +268,20 @@ static int staged_pipeline(const bh_stream* s, int variant, const bh_tune* tune,
     uint32_t* caps_dev = at<uint32_t>(ws, L.caps);
     if ((rc = bh_fill_caps(caps_dev, caps, C, st))) return rc;
     prof_mark(S(st), "tune");
+    stamp_phase(rep, 4, S(st));
     rc = bh_decode_write_classes(s, entries, counts, oi, at<int64_t>(ws, L.perm), nq, 0, maxcap,
                                  at<int64_t>(ws, L.classes), caps_dev, out, s->symbol_count, rep,
                                  stats, st);
     prof_mark(S(st), "decode_write");
+    stamp_phase(rep, 5, S(st));
     return rc;
   }
   uint32_t cap = tune && tune->capacity ? tune->capacity : 3584;
+  stamp_phase(rep, 4, S(st));
   rc = bh_decode_write_classes(s, entries, counts, oi, nullptr, nq, cap, cap, nullptr, nullptr, out,
                                s->symbol_count, rep, stats, st);
   prof_mark(S(st), "decode_write");
+  stamp_phase(rep, 5, S(st));
   return rc;
 }
 
@@ -282,7 +292,9 @@ extern "C" int bh_decode_async(const bh_stream* s, int variant, const bh_tune* t
   if (variant == BH_VARIANT_GAP && !s->gap_dev && s->total_bits) return BH_NOTPRESENT;
   if (s->total_bits && use_fused(s, variant, tune))
     return bh_fused_decode(s, variant, tune, out_dev, ws, ws_bytes, report_dev, cuda_stream);
-  if (s->first_entry) return BH_BAD_ARGUMENT;  // chunked streams: fused path only
+  // chunked streams (first_entry) are fused-path only, and need a 16-byte
+  // aligned payload (shard.chunk_stream cuts at 128-bit multiples)
+  if (s->first_entry) return BH_BAD_ARGUMENT;
   int rc = bh_report_init(report_dev, cuda_stream);
   if (rc) return rc;
   if (s->total_bits == 0) {
@@ -316,7 +328,9 @@ extern "C" int bh_decode(const bh_stream* s, int variant, const bh_tune* tune, u
   if ((rc = bh_report_read(rep, &r, cuda_stream))) return rc;
   if (r.status == BH_NEED_STAGED) {
     // the fused path declined (incomplete codebook): the reference-structured
-    // pipeline reproduces the reference's speculative windows exactly
+    // pipeline reproduces the reference's speculative windows exactly.  It
+    // decodes whole streams only: a chunk (first_entry != 0) cannot take it.
+    if (s->first_entry) return BH_BAD_ARGUMENT;
     if ((rc = bh_report_init(rep, cuda_stream))) return rc;
     if ((rc = staged_pipeline(s, variant, tune, out_dev, ws, need, rep, cuda_stream, true))) return rc;
     if ((rc = bh_report_read(rep, &r, cuda_stream))) return rc;

@@ -232,7 +232,17 @@ struct DevReport {
   unsigned long long seam_passes;   // seam passes that re-seeded something
   unsigned long long repair_needed; // fused sync: seam speculation failed somewhere
   unsigned long long pad[4];
+  unsigned long long phase_ns[6];   // phase boundaries (bh_report.phase_ns)
 };
+
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Host side: stamp phase boundary k of the staged pipeline (stream-ordered).
+int stamp_phase(void* report_dev, int k, cudaStream_t st);
 
 // Host-side phase profiler (abi.cu): when enabled, every decoder phase is
 // bracketed by CUDA events on the launching stream (bh_profile_enable /

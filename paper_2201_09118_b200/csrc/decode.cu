@@ -20,7 +20,15 @@ __global__ void k_report_init(DevReport* rep) {
     rep->write_rounds = rep->staged_slots = rep->bypass_slots = 0;
     rep->total_symbols = rep->stale_seams = rep->seam_passes = rep->repair_needed = 0;
     rep->pad[0] = rep->pad[1] = rep->pad[2] = rep->pad[3] = 0;
+    rep->phase_ns[0] = ~0ull;  // min over CTAs
+    for (int k = 1; k < 6; ++k) rep->phase_ns[k] = 0;
   }
+}
+
+__global__ void k_stamp(DevReport* rep, int k) {
+  const unsigned long long t = global_ns();
+  if (k == 0) atomicMin(&rep->phase_ns[0], t);
+  else atomicMax(&rep->phase_ns[k], t);
 }
 
 // CTA-uniform early exit (one thread reads, everyone agrees).
@@ -569,6 +577,11 @@ extern "C" int bh_device_sm_count(void) { return sm_count(); }
 
 extern "C" size_t bh_report_bytes(void) { return sizeof(DevReport); }
 
+int bh::stamp_phase(void* report_dev, int k, cudaStream_t st) {
+  k_stamp<<<1, 1, 0, st>>>(static_cast<DevReport*>(report_dev), k);
+  return cudaGetLastError() == cudaSuccess ? BH_OK : BH_CUDA_ERROR;
+}
+
 extern "C" int bh_report_init(void* report_dev, void* cuda_stream) {
   k_report_init<<<1, 32, 0, S(cuda_stream)>>>(static_cast<DevReport*>(report_dev));
   return last_status();
@@ -597,6 +610,7 @@ extern "C" int bh_report_read(const void* report_dev, bh_report* out, void* cuda
   out->stale_seams = r.stale_seams;
   out->seam_passes = r.seam_passes;
   out->repair_needed = r.repair_needed;
+  for (int k = 0; k < 6; ++k) out->phase_ns[k] = r.phase_ns[k];
   return BH_OK;
 }
 

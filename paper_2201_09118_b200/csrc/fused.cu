@@ -104,6 +104,7 @@ struct FusedArgs {
   uint32_t wide;         // table layout: 1 = wlut12, 0 = replicated wlut8 (+ lut12 if has_l12)
   uint32_t t_lim, t_c12, t_wp, t_l12;  // shared-memory table offsets (bytes)
   uint32_t t_ljs, ljs_bytes;            // shared copy of ljsym for the limit search (0 bytes: global)
+  uint32_t smem_tiles;                  // ranges up to this many tiles keep their totals in shared memory
   unsigned long long* trace;  // debug timeline (TR instantiation only)
 };
 
@@ -840,6 +841,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
 __device__ __forceinline__ void fused_finish(const FusedArgs& a, uint32_t ep) {
   __syncthreads();
   if (threadIdx.x == 0) {
+    atomicMax(&a.rep->phase_ns[5], global_ns());  // decode_write end (max over CTAs)
     __threadfence();
     const unsigned prev = atomicAdd(a.ws_hdr + 1, 1u);
     if (prev == gridDim.x - 1) {
@@ -942,6 +944,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   __shared__ uint32_t s_wsum[32];
   __shared__ uint32_t s_carry;
   __shared__ uint32_t s_next;  // phase 2: next tile of the range to take
+  __shared__ unsigned long long s_tcount, s_tseam;  // phase clocks (count loop end, seam fix-up end)
   __shared__ uint32_t s_tcnt[MAX_SMEM_TILES];  // symbols per tile of the range (short ranges)
   // SYNC, short ranges: the range's exit descriptors and full-fix flags, so
   // the seam fix-up reads in-range predecessors from shared memory
@@ -965,6 +968,9 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   const uint64_t G = gridDim.x, cta = blockIdx.x;
   const uint64_t t0 = a.nseq * cta / G, t1 = a.nseq * (cta + 1) / G;
   const uint32_t nt = (uint32_t)(t1 - t0);
+  // short ranges keep tile totals / seam descriptors in shared memory; long
+  // ranges (or a forced BH_FUSED_SMEM_TILES) use the workspace copies
+  const bool srange = nt <= a.smem_tiles;
   bool bad = false;
 
   const uint32_t sm_s = smem_u32(sm);
@@ -1014,7 +1020,13 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   T.max_len = hdr->max_len ? min(hdr->max_len, 32u) : 32u;
   if (VAR == BH_VARIANT_SYNC)
     for (uint32_t i = threadIdx.x; i < SX; i += blockDim.x) { s_texit[i] = 0; s_tff[i] = 0; }
-  if (threadIdx.x == 0) s_next = W;  // phase 2 starts with tile t0 + warp index
+  if (threadIdx.x == 0) {
+    s_next = W;  // phase 2 starts with tile t0 + warp index
+    s_tcount = s_tseam = 0;
+    const unsigned long long t = global_ns();
+    atomicMin(&a.rep->phase_ns[0], t);
+    if (VAR == BH_VARIANT_GAP) atomicMax(&a.rep->phase_ns[1], t);  // entries come from the gap bytes inline
+  }
   __syncthreads();  // barriers initialised
   MARK(56);
   mbar_wait(bar_ct, 0);
@@ -1024,7 +1036,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   // SYNC: first-slot candidate counts of this warp's tiles in its (still
   // unused) staging buffer when they fit, else in the workspace
   const uint32_t ktiles = t0 + wib < t1 ? (uint32_t)((t1 - (t0 + wib) + W - 1) / W) : 0u;
-  const bool scand = VAR == BH_VARIANT_SYNC && nt <= MAX_SMEM_TILES && 64 * ktiles <= 2 * a.cap;
+  const bool scand = VAR == BH_VARIANT_SYNC && srange && 64 * ktiles <= 2 * a.cap;
   uint32_t kidx = 0;
   // GAP: the gap bytes of a tile are loaded one tile ahead, like its words
   auto gap_load = [&](uint64_t t, uint32_t* g) {
@@ -1060,7 +1072,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       else a.cand[tile * 32 + lane] = (uint16_t)min(cand, 0xffffu);
       if (lane == 0) {
         a.tile_dlt[tile] = fullfix ? FULL_FIX : 0;
-        if (nt <= MAX_SMEM_TILES) {
+        if (srange) {
           s_tff[tile - t0] = fullfix ? 1 : 0;
           *(volatile unsigned long long*)&s_texit[tile - t0] = dsc;
         }
@@ -1077,7 +1089,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     if (de > 0xffffu || incl > 0xffffu) bad = true;
     a.lane_info[tile * 32 + lane] = (de & 0xffffu) | ((incl - c) << 16);
     if (lane == 31) {
-      if (nt <= MAX_SMEM_TILES) s_tcnt[tile - t0] = incl;
+      if (srange) s_tcnt[tile - t0] = incl;
       else a.tile_cnt[tile] = incl;
     }
     wb_a = wb_b;
@@ -1085,6 +1097,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   }
   cp_wait<0>();
   __syncwarp();  // candidate slots written by other lanes are read below
+  if (lane == 0) atomicMax(&s_tcount, global_ns());
   MARK(9);
   if (VAR == BH_VARIANT_SYNC) {
     // Seam fix-up (inter_sync, sync_decoder.py:116-149).  Every exit that does
@@ -1102,7 +1115,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       if (!__any_sync(0xffffffffu, mine)) break;
       bool serial = false;
       if (mine && tk > 0) {
-        const bool sm_own = nt <= MAX_SMEM_TILES, sm_pred = sm_own && tk - 1 >= t0;
+        const bool sm_own = srange, sm_pred = sm_own && tk - 1 >= t0;
         unsigned long long dp;
         const unsigned long long ds = sm_own ? *(volatile unsigned long long*)&s_texit[tk - t0]
                                              : ld_relaxed(a.exit_desc + tk);
@@ -1122,7 +1135,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
                                      : (int32_t)a.cand[tk * 32 + o] - (int32_t)a.cand[tk * 32];
             a.tile_dlt[tk] = dl;
             a.lane_info[tk * 32] = o;  // first slot enters at the seed; prefix 0
-            if (nt <= MAX_SMEM_TILES) s_tcnt[tk - t0] += (uint32_t)dl;
+            if (srange) s_tcnt[tk - t0] += (uint32_t)dl;
             else a.tile_cnt[tk] += (uint32_t)dl;
           } else {
             a.tile_dlt[tk] = 0;
@@ -1138,7 +1151,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         const uint32_t j = __ffs(sm_mask) - 1;
         sm_mask &= sm_mask - 1;
         const uint64_t st = t0 + wib + (kb + j) * W;
-        const bool sm_own = nt <= MAX_SMEM_TILES, sm_pred = sm_own && st - 1 >= t0;
+        const bool sm_own = srange, sm_pred = sm_own && st - 1 >= t0;
         unsigned long long dp = 0;
         if (lane == 0) {
           if (sm_pred) {
@@ -1163,7 +1176,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
                                      : (int32_t)a.cand[st * 32 + o] - (int32_t)a.cand[st * 32];
             a.tile_dlt[st] = dl;
             a.lane_info[st * 32] = o;
-            if (nt <= MAX_SMEM_TILES) s_tcnt[st - t0] += (uint32_t)dl;
+            if (srange) s_tcnt[st - t0] += (uint32_t)dl;
             else a.tile_cnt[st] += (uint32_t)dl;
           }
           __syncwarp();
@@ -1182,7 +1195,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         unsigned long long dsc = 0;
         tile_counts<VAR>(a, T, st, dbuf_s, wbs, nsl, ep, e, c, bad, (int32_t)min(o, 255u), nullptr, nullptr,
                          nullptr, &dsc);
-        if (lane == 0 && nt <= MAX_SMEM_TILES) *(volatile unsigned long long*)&s_texit[st - t0] = dsc;
+        if (lane == 0 && srange) *(volatile unsigned long long*)&s_texit[st - t0] = dsc;
         uint32_t incl = c;
         for (int off = 1; off < 32; off <<= 1) {
           const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
@@ -1194,13 +1207,14 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         a.lane_info[st * 32 + lane] = (de & 0xffffu) | ((incl - c) << 16);
         if (lane == 31) {
           a.tile_dlt[st] = 0;
-          if (nt <= MAX_SMEM_TILES) s_tcnt[st - t0] = incl;
+          if (srange) s_tcnt[st - t0] = incl;
           else a.tile_cnt[st] = incl;
         }
         __syncwarp();
       }
     }
   }
+  if (VAR == BH_VARIANT_SYNC && lane == 0) atomicMax(&s_tseam, global_ns());
   MARK(2);
 
   // ---- tile offsets within the range, CTA aggregate -----------------------
@@ -1210,8 +1224,12 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     for (uint32_t i = threadIdx.x; i < 256 * 8; i += blockDim.x)
       sts128(sm_s + 16 * i, lds128(sm_s + a.t_wp + 16 * (i >> 3)));
   __syncthreads();  // tile totals and the replicated decode table visible
+  if (threadIdx.x == 0) {
+    atomicMax(&a.rep->phase_ns[VAR == BH_VARIANT_GAP ? 2 : 1], s_tcount);
+    if (VAR == BH_VARIANT_SYNC) atomicMax(&a.rep->phase_ns[2], s_tseam);
+  }
   uint32_t carry = 0;
-  if (nt <= MAX_SMEM_TILES) {
+  if (srange) {
     // each warp sums the totals before its tiles itself (phase 2); warp 0 the aggregate
     if (wib == 0) {
       uint32_t v = 0;
@@ -1260,6 +1278,9 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       if (lane == 0) st_relaxed(a.cnt_desc + cta, mkdesc(ep, D_INC, excl + carry));
     }
     if (lane == 0) {
+      const unsigned long long tr = global_ns();  // output index resolved (count_pass / output_index end)
+      atomicMax(&a.rep->phase_ns[3], tr);
+      atomicMax(&a.rep->phase_ns[4], tr);
       s_ctaoff = excl;
       if (cta == G - 1) {
         a.rep->total_symbols = excl + carry;
@@ -1301,7 +1322,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       if (VAR == BH_VARIANT_SYNC) dlt_n = a.tile_dlt[tn];
     }
     uint32_t C, toff;
-    if (nt <= MAX_SMEM_TILES) {
+    if (srange) {
       const uint32_t ti = (uint32_t)(tile - t0);
       uint32_t v = 0;
       for (uint32_t i = lane; i < ti; i += 32) v += s_tcnt[i];
@@ -1537,6 +1558,8 @@ extern "C" int bh_fused_supported(const bh_stream* s, int variant) {
   if (env_int("BH_DISABLE_FUSED", 0)) return 0;
   if (variant != BH_VARIANT_GAP && variant != BH_VARIANT_SYNC) return 0;
   if (s->subseqs_per_seq == 0) return 0;
+  // words are staged with 16-byte cp.async: the payload must be 16-byte aligned
+  if (reinterpret_cast<uintptr_t>(s->words_dev) & 15u) return 0;
   const uint64_t seq_bits = (uint64_t)vsb_of(s) * TILE_SUBSEQ;
   if (seq_bits > 16384 || s->total_bits >= (1ull << 36) || s->symbol_count >= (1ull << 36)) return 0;
   if (variant == BH_VARIANT_GAP && !s->gap_dev) return 0;
@@ -1601,24 +1624,30 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.t_l12 = cfg.t_l12;
   a.t_ljs = cfg.t_ljs;
   a.ljs_bytes = cfg.ljs_bytes;
+  a.smem_tiles = (uint32_t)env_int("BH_FUSED_SMEM_TILES", (int)MAX_SMEM_TILES);
+  if (a.smem_tiles > MAX_SMEM_TILES) a.smem_tiles = MAX_SMEM_TILES;
   const int sms = device_sm_count();
   a.trace = g_trace.load(std::memory_order_relaxed);
   const void* fn =
       variant == BH_VARIANT_GAP ? (a.trace ? (const void*)k_fused2<BH_VARIANT_GAP, 1> : (const void*)k_fused2<BH_VARIANT_GAP, 0>)
                                 : (a.trace ? (const void*)k_fused2<BH_VARIANT_SYNC, 1> : (const void*)k_fused2<BH_VARIANT_SYNC, 0>);
-  // launch attributes and occupancy cached per (kernel, threads, smem)
+  // launch attributes and occupancy cached per (device, kernel, threads,
+  // smem): the dynamic shared-memory opt-in is a per-device (per-context)
+  // function attribute
   static std::mutex mu;
-  static std::map<std::tuple<const void*, uint32_t, uint32_t>, int> occ;
+  static std::map<std::tuple<int, const void*, uint32_t, uint32_t>, int> occ;
   int per_sm = 0;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return BH_CUDA_ERROR;
   {
     std::lock_guard<std::mutex> g(mu);
-    auto key = std::make_tuple(fn, cfg.warps, cfg.smem);
+    auto key = std::make_tuple(dev, fn, cfg.warps, cfg.smem);
     auto it = occ.find(key);
     if (it == occ.end()) {
-      // the attribute is per kernel: raise it to the largest size ever cached
-      // (lowering it would break a cached larger configuration)
-      static std::map<const void*, uint32_t> smem_set;
-      uint32_t& cur = smem_set[fn];
+      // the attribute is per kernel and device: raise it to the largest size
+      // ever cached there (lowering it would break a cached larger configuration)
+      static std::map<std::pair<int, const void*>, uint32_t> smem_set;
+      uint32_t& cur = smem_set[std::make_pair(dev, fn)];
       if (cfg.smem > cur) {
         if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cfg.smem) != cudaSuccess)
           return BH_CUDA_ERROR;
@@ -1635,6 +1664,11 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   uint64_t grid = (uint64_t)per_sm * sms;
   const uint64_t need = (nseq + cfg.warps - 1) / cfg.warps;  // groups
   if (grid > need) grid = need;
+  // caller-chosen CTA count (concurrent decodes sharing the GPU)
+  if (tune && tune->ctas && tune->ctas < grid) grid = tune->ctas;
+  // test knob: fewer CTAs, i.e. longer per-CTA tile ranges
+  const int gforce = env_int("BH_FUSED_GRID", 0);
+  if (gforce > 0 && (uint64_t)gforce < grid) grid = (uint64_t)gforce;
   if (grid < 1) grid = 1;
   prof_mark(static_cast<cudaStream_t>(cuda_stream), "start");
   void* args[] = {&a};

@@ -280,6 +280,214 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// K1 fast path for canonical books (bh_table_build): ONE launch of a few CTAs.
+// Every CTA rebuilds the canonical order of the <= 4096 codes of length <= 12
+// in shared memory from the length bytes (codebook.py:86-112: counting sort by
+// (length, symbol), first_code/first_index per length, codebook.py:209-233),
+// then fills its slice of the direct tables.  A codeword is found from a
+// 32-bit window by the canonical limits (the first length whose left-justified
+// limit exceeds the window, a 5-step search over 33 shared values) and its
+// symbol by base[len] + code -- no per-entry global binary search.
+// ---------------------------------------------------------------------------
+constexpr int K1_THREADS = 512;
+constexpr int K1_GRID = 16;
+
+struct CanonSmem {
+  unsigned long long lim[33];
+  long long base[33];
+  uint32_t count[33];
+  uint32_t fill[33];
+  uint32_t wcnt[K1_THREADS / 32][33];
+  uint16_t sym[FB_SIZE];  // canonical order of the codes of length <= 12
+  int bad;
+};
+
+// sym | len<<16 of the codeword at the front of `win`; len only (sym 0) for
+// codes longer than 12 bits; 0 when no codeword matches (incomplete book)
+__device__ __forceinline__ uint32_t canon_one(const CanonSmem& S, uint32_t win) {
+  if ((unsigned long long)win >= S.lim[32]) return 0u;
+  uint32_t lo = 1, hi = 32;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if ((unsigned long long)win < S.lim[mid]) hi = mid; else lo = mid + 1;
+  }
+  if (lo > (uint32_t)FB) return lo << 16;
+  const long long idx = S.base[lo] + (long long)(win >> (32 - lo));
+  return (uint32_t)S.sym[idx] | (lo << 16);
+}
+
+// symbol k (0..5) of a multi-symbol entry into its halfword of x|y|z
+__device__ __forceinline__ void pack6(uint32_t& x, uint32_t& y, uint32_t& z, uint32_t k, uint32_t sym) {
+  const uint32_t v = sym << ((k & 1u) * 16);
+  if (k < 2) x |= v; else if (k < 4) y |= v; else z |= v;
+}
+
+__global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __restrict__ lengths, uint32_t alphabet,
+                                                           void* blob, uint32_t max_codes) {
+  __shared__ CanonSmem S;
+  TableHdr* hdr; uint32_t* lut; uint16_t* cnt; uint32_t* lj; uint16_t* ljsym; uint8_t* ljlen;
+  table_ptrs(blob, max_codes, hdr, lut, cnt, lj, ljsym, ljlen);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t G = gridDim.x, cta = blockIdx.x;
+  if (tid < 33) { S.count[tid] = 0; S.fill[tid] = 0; }
+  if (tid == 0) S.bad = 0;
+  __syncthreads();
+  for (uint32_t s = tid; s < alphabet; s += K1_THREADS) {
+    const uint32_t ln = lengths[s];
+    if (ln > 32) S.bad = 1;
+    else if (ln) atomicAdd(&S.count[ln], 1u);
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long code = 0, kraft = 0;
+    uint32_t idx = 0, ml = 0;
+    S.lim[0] = 0;
+    S.base[0] = 0;
+#pragma unroll 1
+    for (int ln = 1; ln <= 32; ++ln) {
+      const uint32_t c = S.count[ln];
+      S.lim[ln] = (code + c) << (32 - ln);
+      S.base[ln] = (long long)idx - (long long)code;
+      S.fill[ln] = idx;  // first_index: rank base of the length
+      code = (code + c) << 1;
+      idx += c;
+      kraft += (unsigned long long)c << (32 - ln);
+      if (c) ml = ln;
+    }
+    if (idx > max_codes) S.bad = 1;
+    if (cta == 0) {
+      hdr->kind = 0;
+      hdr->max_len = ml;
+      hdr->ncodes = idx;
+      hdr->lut_bits = LUT_BITS;
+      hdr->alphabet = alphabet;
+      hdr->status = S.bad ? BH_BAD_ARGUMENT : BH_OK;
+      hdr->complete = kraft == (1ull << 32) ? 1u : 0u;
+      TableLayout L(max_codes);
+      unsigned long long* glim = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(blob) + L.lim);
+      long long* gbase = reinterpret_cast<long long*>(reinterpret_cast<char*>(blob) + L.base);
+#pragma unroll 1
+      for (int ln = 0; ln <= 32; ++ln) { glim[ln] = S.lim[ln]; gbase[ln] = S.base[ln]; }
+    }
+  }
+  __syncthreads();
+  if (S.bad) return;
+  // ranks: counting sort by (length, symbol); S.fill[ln] = next free index
+  const unsigned lt = (1u << lane) - 1;
+  for (uint32_t b0 = 0; b0 < alphabet; b0 += K1_THREADS) {
+    const uint32_t s = b0 + tid;
+    const uint32_t ln = s < alphabet ? lengths[s] : 0u;
+    const unsigned peers = __match_any_sync(0xffffffffu, ln);
+    const uint32_t wrank = __popc(peers & lt);
+    for (int i = lane; i < 33; i += 32) S.wcnt[warp][i] = 0;
+    __syncwarp();
+    if (ln && wrank == 0) S.wcnt[warp][ln] = __popc(peers);
+    __syncthreads();
+    if (ln) {
+      uint32_t r = S.fill[ln] + wrank;
+      for (int w = 0; w < warp; ++w) r += S.wcnt[w][ln];
+      if (ln <= (uint32_t)FB && r < FB_SIZE) S.sym[r] = (uint16_t)s;
+      // the global long-code arrays: one CTA per 1024-symbol block
+      if ((b0 / K1_THREADS) % G == cta) {
+        const long long code = (long long)r - S.base[ln];
+        lj[r] = (uint32_t)((unsigned long long)code << (32 - ln));
+        ljsym[r] = (uint16_t)s;
+        ljlen[r] = (uint8_t)ln;
+      }
+    }
+    __syncthreads();
+    if (tid >= 1 && tid <= 32) {
+      uint32_t add = 0;
+      for (int w = 0; w < K1_THREADS / 32; ++w) add += S.wcnt[w][tid];
+      S.fill[tid] += add;
+    }
+    __syncthreads();
+  }
+  // direct tables: 12-bit (lut12, clut12, wlut12), 11-bit (lut, cnt) and
+  // 8-bit (dlut8, clut8, wlut8) entries spread over every thread of the grid
+  TableLayout L(max_codes);
+  char* B = static_cast<char*>(blob);
+  uint32_t* lut12 = reinterpret_cast<uint32_t*>(B + L.lut12);
+  uint16_t* clut12 = reinterpret_cast<uint16_t*>(B + L.clut12);
+  uint4* wlut12 = reinterpret_cast<uint4*>(B + L.wlut12);
+  uint32_t* dlut8 = reinterpret_cast<uint32_t*>(B + L.dlut8);
+  uint8_t* clut8 = reinterpret_cast<uint8_t*>(B + L.clut8);
+  uint4* wlut8 = reinterpret_cast<uint4*>(B + L.wlut8);
+  constexpr uint32_t N12 = FB_SIZE, N11 = LUT_SIZE, N8 = 256;
+  for (uint32_t it = cta * K1_THREADS + tid; it < N12 + N11 + N8; it += G * K1_THREADS) {
+    if (it < N12) {
+      const uint32_t v = it;
+      const uint32_t w0 = v << (32 - FB);
+      const uint32_t e0 = canon_one(S, w0);
+      lut12[v] = ((e0 >> 16) & 0xffu) <= (uint32_t)FB ? e0 : 0u;
+      // every whole codeword of the 12-bit window (zero fill past it cannot
+      // change a match that lies inside it): start mask and end; the first six
+      // also for the multi-symbol decode table
+      uint32_t pos = 0, starts = 0, n6 = 0, l0 = 0, p6 = 0, sx = 0, sy = 0, sz = 0;
+      while (pos < (uint32_t)FB) {
+        const uint32_t e = pos ? canon_one(S, w0 << pos) : e0;
+        const uint32_t len = (e >> 16) & 0xffu;
+        if (len == 0 || pos + len > (uint32_t)FB) break;
+        starts |= 1u << pos;
+        if (n6 < 6) {
+          if (n6 == 0) l0 = len;
+          pack6(sx, sy, sz, n6++, e & 0xffffu);
+          p6 = pos + len;
+        }
+        pos += len;
+      }
+      clut12[v] = (uint16_t)(starts | (pos << 12));
+      uint4 wl;
+      wl.x = sx;
+      wl.y = sy;
+      wl.z = sz;
+      wl.w = n6 ? (p6 | (n6 << 4) | (l0 << 16) | ((2 * n6) << 28)) : 0u;
+      wlut12[v] = wl;
+    } else if (it < N12 + N11) {
+      const uint32_t v = it - N12;
+      const uint32_t w0 = v << (32 - LUT_BITS);
+      const uint32_t e0 = canon_one(S, w0);
+      lut[v] = ((e0 >> 16) & 0xffu) <= (uint32_t)LUT_BITS ? e0 : 0u;
+      uint32_t pos = 0, n = 0;
+      while (pos < (uint32_t)LUT_BITS) {
+        const uint32_t e = pos ? canon_one(S, w0 << pos) : e0;
+        const uint32_t len = (e >> 16) & 0xffu;
+        if (len == 0 || pos + len > (uint32_t)LUT_BITS) break;
+        pos += len;
+        ++n;
+      }
+      cnt[v] = n ? (uint16_t)(pos | (n << 8)) : (uint16_t)0;
+    } else {
+      const uint32_t v = it - N12 - N11;
+      const uint32_t w0 = v << 24;
+      const uint32_t e0 = canon_one(S, w0);
+      dlut8[v] = ((e0 >> 16) & 0xffu) <= 8u ? e0 : 0u;
+      uint32_t pos = 0, n = 0, n6 = 0, p6 = 0, l0 = 0, sx = 0, sy = 0, sz = 0;
+      while (pos < 8) {
+        const uint32_t e = pos ? canon_one(S, w0 << pos) : e0;
+        const uint32_t len = (e >> 16) & 0xffu;
+        if (len == 0 || pos + len > 8) break;
+        if (n6 < 6) {
+          if (n6 == 0) l0 = len;
+          pack6(sx, sy, sz, n6++, e & 0xffffu);
+          p6 = pos + len;
+        }
+        pos += len;
+        ++n;
+      }
+      clut8[v] = n ? (uint8_t)((n << 3) | (pos - 1)) : (uint8_t)0;
+      uint4 wl;
+      wl.x = sx;
+      wl.y = sy;
+      wl.z = sz;
+      wl.w = n6 ? (p6 | (n6 << 4) | (n << 8) | (pos << 12) | (l0 << 16) | ((2 * n6) << 28)) : 0u;
+      wlut8[v] = wl;
+    }
+  }
+}
+
 }  // namespace bh
 
 using namespace bh;
@@ -293,8 +501,7 @@ extern "C" int bh_table_build(const uint8_t* lengths_dev, uint32_t alphabet, voi
   if (!table_dev || (alphabet && !lengths_dev) || alphabet > 65536u || max_codes > 65536u)
     return BH_BAD_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-  k_canonical<<<1, 1024, 0, st>>>(lengths_dev, alphabet, table_dev, max_codes, nullptr);
-  k_fill_luts<<<1, 1024, 0, st>>>(table_dev, max_codes);
+  k_table_canon<<<K1_GRID, K1_THREADS, 0, st>>>(lengths_dev, alphabet, table_dev, max_codes);
   return cuda_status(cudaGetLastError());
 }
 

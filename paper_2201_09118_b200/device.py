@@ -10,6 +10,7 @@ decodes of one stream upload nothing.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 
 import numpy as np
 
@@ -52,21 +53,34 @@ def zeros(n: int, dtype, device):
 
 
 class Workspace:
-    """Grow-only device scratch shared by the calls of one process."""
+    """Grow-only device scratch, one buffer per (device, CUDA stream, tag).
+
+    The C ABI is safe per (workspace, stream) pair (include/b200huff.h): calls
+    on one stream are ordered, so they may share a workspace; calls on
+    different streams -- e.g. two host threads, each on its own stream -- get
+    different buffers.  The reference decoders are safe for concurrent callers
+    (staging.py:48-62), and so is this mirror.  The map is guarded by a lock;
+    a buffer that grows is replaced, and the old one stays alive until the
+    work already queued on its stream has finished with it (torch's caching
+    allocator orders its reuse on that stream)."""
 
     _bufs: dict = {}
+    _lock = threading.Lock()
 
     @classmethod
     def get(cls, nbytes: int, device, tag: str = "main"):
         torch = require_cuda()
-        key = (str(device), tag)
-        buf = cls._bufs.get(key)
-        if buf is None or buf.numel() < nbytes:
-            buf = torch.empty(max(int(nbytes), 256) + 256, dtype=torch.uint8, device=device)
-            # fused-kernel descriptors are epoch-tagged: zero once per allocation
-            check(load().bh_workspace_reset(buf.data_ptr(), buf.numel(), stream_handle()), "workspace")
-            cls._bufs[key] = buf
-        return buf
+        dev = torch.device(device)
+        st = torch.cuda.current_stream(dev)
+        key = (str(dev), st.cuda_stream, tag)
+        with cls._lock:
+            buf = cls._bufs.get(key)
+            if buf is None or buf.numel() < nbytes:
+                buf = torch.empty(max(int(nbytes), 256) + 256, dtype=torch.uint8, device=dev)
+                # fused-kernel descriptors are epoch-tagged: zero once per allocation
+                check(load().bh_workspace_reset(buf.data_ptr(), buf.numel(), stream_handle(st)), "workspace")
+                cls._bufs[key] = buf
+            return buf
 
 
 class DeviceStream:
@@ -125,16 +139,26 @@ class DeviceStream:
         return self.stream.num_seqs
 
 
+_ds_lock = threading.Lock()
+
+
 def device_stream(stream, device=None) -> DeviceStream:
+    """The stream's device mirror on `device`, built once and cached on the
+    EncodedStream.  Its uploads and table build are queued on the stream that
+    built it; a caller on another CUDA stream waits for them (an event)."""
     torch = require_cuda()
     dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
     cache = getattr(stream, "_device", None)
     key = str(dev)
-    if isinstance(cache, dict) and key in cache:
-        return cache[key]
-    ds = DeviceStream(stream, dev)
-    if isinstance(cache, dict):
-        cache[key] = ds
+    with _ds_lock:
+        ds = cache.get(key) if isinstance(cache, dict) else None
+        if ds is None:
+            ds = DeviceStream(stream, dev)
+            ds.ready = torch.cuda.Event()
+            ds.ready.record(torch.cuda.current_stream(dev))
+            if isinstance(cache, dict):
+                cache[key] = ds
+    torch.cuda.current_stream(dev).wait_event(ds.ready)
     return ds
 
 

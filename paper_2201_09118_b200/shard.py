@@ -100,6 +100,24 @@ class Chunk:
     out0: int
 
 
+def _chunk(q0: int, q1: int, total_bits: int, subseq_bits: int, subseqs_per_seq: int, gap, oi) -> "Chunk":
+    nsub = -(-total_bits // subseq_bits)
+    seq_bits = subseq_bits * subseqs_per_seq
+    s0, s1 = q0 * subseqs_per_seq, min(q1 * subseqs_per_seq, nsub)
+    b0 = q0 * seq_bits
+    end = total_bits if s1 >= nsub else min(s1 * subseq_bits + int(gap[s1]), total_bits)
+    tb = end - b0
+    ns = -(-tb // subseq_bits)
+    return Chunk(q0, q1, b0 // 32, tb, s0, ns, int(gap[s0]) if s0 else 0, int(oi[s1] - oi[s0]), int(oi[s0]))
+
+
+def _check_chunkable(subseq_bits: int, subseqs_per_seq: int) -> None:
+    if (subseq_bits * subseqs_per_seq) % 128:
+        # a chunk's payload pointer (words + word0) must stay 16-byte aligned:
+        # the fused kernel stages words with 16-byte cp.async
+        raise ValueError("chunking needs sequences that are a whole number of 128-bit (16-byte) blocks")
+
+
 def chunk_stream(total_bits: int, subseq_bits: int, subseqs_per_seq: int, gap, subseq_counts,
                  nchunks: int) -> list[Chunk]:
     """Cut a stream into `nchunks` sequence-aligned chunks.
@@ -108,23 +126,46 @@ def chunk_stream(total_bits: int, subseq_bits: int, subseqs_per_seq: int, gap, s
     per subsequence (the gap count pass), both recorded at encode time; they
     give every chunk's entry bit and symbol count without decoding.
     """
+    _check_chunkable(subseq_bits, subseqs_per_seq)
     gap = np.asarray(gap, dtype=np.int64)
     cnt = np.asarray(subseq_counts, dtype=np.int64)
     nsub = -(-total_bits // subseq_bits)
     nseq = -(-nsub // subseqs_per_seq)
-    seq_bits = subseq_bits * subseqs_per_seq
-    if seq_bits % 32:
-        raise ValueError("chunking needs sequences that are a whole number of 32-bit words")
     oi = np.concatenate([[0], np.cumsum(cnt)])
-    out = []
-    for q0, q1 in sequence_ranges(nseq, max(1, min(nchunks, nseq))):
-        if q0 == q1:
-            continue
-        s0, s1 = q0 * subseqs_per_seq, min(q1 * subseqs_per_seq, nsub)
-        b0 = q0 * seq_bits
-        end = total_bits if s1 >= nsub else min(s1 * subseq_bits + int(gap[s1]), total_bits)
-        tb = end - b0
-        ns = -(-tb // subseq_bits)
-        out.append(Chunk(q0, q1, b0 // 32, tb, s0, ns, int(gap[s0]) if s0 else 0,
-                         int(oi[s1] - oi[s0]), int(oi[s0])))
+    return [_chunk(q0, q1, total_bits, subseq_bits, subseqs_per_seq, gap, oi)
+            for q0, q1 in sequence_ranges(nseq, max(1, min(nchunks, nseq))) if q0 < q1]
+
+
+def balanced_pieces(num_seqs, world: int) -> list[list[tuple[int, int, int]]]:
+    """Strong-scaling split of a batch of fields over `world` ranks.
+
+    The fields' sequences are laid end to end and cut into `world` contiguous
+    spans of equal sequence count (every sequence holds the same number of
+    payload bits, and decode time follows payload bits across the batch's
+    compression ratios); each span becomes at most one piece per field it
+    touches.  Returns, per rank, [(field, q0, q1)] -- far fewer launches per
+    rank than an LPT spread of many small chunks.
+    """
+    if world < 1:
+        raise ValueError("world must be >= 1")
+    starts = np.concatenate([[0], np.cumsum(np.asarray(num_seqs, dtype=np.int64))])
+    total = int(starts[-1])
+    out: list[list[tuple[int, int, int]]] = []
+    for r in range(world):
+        g0, g1 = total * r // world, total * (r + 1) // world
+        mine = []
+        for f in range(len(num_seqs)):
+            lo, hi = max(g0, int(starts[f])), min(g1, int(starts[f + 1]))
+            if lo < hi:
+                mine.append((f, lo - int(starts[f]), hi - int(starts[f])))
+        out.append(mine)
     return out
+
+
+def piece_chunk(total_bits: int, subseq_bits: int, subseqs_per_seq: int, gap, subseq_counts,
+                q0: int, q1: int) -> Chunk:
+    """The sequence range [q0, q1) of one stream as a decodable Chunk."""
+    _check_chunkable(subseq_bits, subseqs_per_seq)
+    gap = np.asarray(gap, dtype=np.int64)
+    oi = np.concatenate([[0], np.cumsum(np.asarray(subseq_counts, dtype=np.int64))])
+    return _chunk(q0, q1, total_bits, subseq_bits, subseqs_per_seq, gap, oi)

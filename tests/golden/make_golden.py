@@ -8,6 +8,8 @@ Run in the build container only (it imports parhuff from
 Outputs (committed):
   tests/golden/cases/<name>.npz  -- stream + every reference output the tests pin
   tests/golden/digests.json      -- sha256 digests for full-size synthetic fields
+                                    (`--digests [keys]`: only these, every
+                                    BASELINE config by default)
 
 The cases mirror the reference's own tests: the Listing-1
 worked streams, deep/long codes, trailing windows without a start, aligned
@@ -265,23 +267,38 @@ def main():
                               gap=z["gap"] if int(z["has_gap"]) else None)
         ph.write_container(st, cdir / f"{name}.huf2")
 
-    digests = {}
-    for key in ("1m", "hurricane"):
+    make_digests(("1m", "hurricane"))
+
+
+# every BASELINE.json config (SURVEY §8d shapes): the reference encoder's bytes
+DIGEST_KEYS = ("1m", "hurricane", "nyx", "nyx256", "nyx4096", "hacc", "cesm", "rtm", "qmcpack")
+
+
+def make_digests(keys=DIGEST_KEYS):
+    """sha256 of the reference encoder's output (lengths, units, gap) and of the
+    symbols for full-size synthetic fields; the reference gap decoder checks
+    each stream round-trips.  Existing entries for other keys are kept."""
+    path = HERE / "digests.json"
+    digests = json.loads(path.read_text()) if path.exists() else {}
+    for key in keys:
         spec = FIELDS[key]
         codes = field_codes(spec)
         book = book_for(codes, 16)
         stream = ph.encode(codes, book, ph.DEFAULT_LAYOUT, with_gap=True)
         _, lens = book.encode_arrays()
-        dec = gap_decoder.decode(stream, workers=8)
+        dec = gap_decoder.decode(stream, workers=os.cpu_count() or 8)
         assert np.array_equal(dec, codes)
         digests[key] = {
             "n": spec.n, "total_bits": int(stream.total_bits), "max_len": int(book.max_len),
             "lengths": sha(lens), "units": sha(stream.units), "gap": sha(stream.gap),
             "symbols": sha(codes),
         }
-        print(key, digests[key])
-    (HERE / "digests.json").write_text(json.dumps(digests, indent=1) + "\n")
-
+        print(key, digests[key], flush=True)
+        del codes, stream, dec
+        path.write_text(json.dumps(digests, indent=1) + "\n")
 
 if __name__ == "__main__":
-    main()
+    if len(sys.argv) > 1 and sys.argv[1] == "--digests":
+        make_digests(tuple(sys.argv[2:]) or DIGEST_KEYS)
+    else:
+        main()

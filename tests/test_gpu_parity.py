@@ -177,18 +177,69 @@ def test_mis_sync_worked_example(ph):
     assert "".join(chr(s) for s in ph.mis_sync_decode(st, 1)) == "CAABCBA"
 
 
-def test_full_size_hurricane_and_1m_digests(ph):
-    """Reference encoder's bytes for the bench configs, then both decoders."""
+FULL_KEYS = ("1m", "hurricane", "nyx", "nyx256", "nyx4096", "hacc", "cesm", "rtm", "qmcpack")
+
+
+@pytest.mark.parametrize("key", FULL_KEYS)
+def test_full_size_config_digests(ph, key):
+    """Every BASELINE.json config at full size: the reference encoder's bytes
+    (sha256 of lengths, units, gap written by make_golden.py --digests from the
+    real parhuff), then both decoders bit-exact on the device (compared there,
+    so the 562 MB HACC output never crosses PCIe)."""
+    import torch
     from paper_2201_09118_b200.synth import FIELDS, field_codes
-    dg = digests()
-    for key in ("1m", "hurricane"):
-        d = dg[key]
-        codes = field_codes(FIELDS[key])
-        assert hashlib.sha256(codes.tobytes()).hexdigest() == d["symbols"]
-        book = ph.book_for(codes, 16)
-        st = ph.encode(codes, book, ph.DEFAULT_LAYOUT, with_gap=True)
-        assert st.total_bits == d["total_bits"]
-        assert hashlib.sha256(st.units.tobytes()).hexdigest() == d["units"]
-        assert hashlib.sha256(st.gap.tobytes()).hexdigest() == d["gap"]
-        assert np.array_equal(ph.gap_decoder.decode(st), codes)
-        assert np.array_equal(ph.sync_decoder.decode(st), codes)
+    d = digests()[key]
+    codes = field_codes(FIELDS[key])
+    assert codes.size == d["n"]
+    assert hashlib.sha256(codes.tobytes()).hexdigest() == d["symbols"]
+    book = ph.book_for(codes, 16)
+    _, lens = book.encode_arrays()
+    assert book.max_len == d["max_len"]
+    assert hashlib.sha256(lens.tobytes()).hexdigest() == d["lengths"]
+    st = ph.encode(codes, book, ph.DEFAULT_LAYOUT, with_gap=True)
+    assert st.total_bits == d["total_bits"]
+    assert hashlib.sha256(st.units.tobytes()).hexdigest() == d["units"]
+    assert hashlib.sha256(st.gap.tobytes()).hexdigest() == d["gap"]
+    want = torch.from_numpy(codes.view(np.int16)).cuda()
+    for dec in (ph.gap_decoder, ph.sync_decoder):
+        got = dec.decode(st, device_out=True)
+        assert got.numel() == codes.size
+        assert torch.equal(got, want), (key, dec.__name__)
+        del got
+    st._device = {}  # release the device copy before the next config
+
+
+@pytest.mark.parametrize("key", ("1m", "hurricane", "hacc"))
+def test_coarse_baseline_k8(ph, key):
+    """K8, the in-run cuSZ-style coarse decoder (one thread per fixed-symbol
+    chunk, encoder-recorded chunk offsets): bit-exact at every chunk size of
+    the SURVEY §8d sweep (2^8 .. 2^14 symbols), against the codes and the
+    single-cursor truth (encoder.py:129-159)."""
+    import torch
+    from paper_2201_09118_b200 import _lib
+    from paper_2201_09118_b200._lib import check, stream_handle
+    from paper_2201_09118_b200.device import DeviceReport, device_stream, empty, h2d
+    from paper_2201_09118_b200.encoder import encode_device
+    from paper_2201_09118_b200.synth import FIELDS, field_codes
+    codes = field_codes(FIELDS[key], n=min(FIELDS[key].n, 40_000_000))
+    book = ph.book_for(codes, 16)
+    st = ph.encode(codes, book, ph.DEFAULT_LAYOUT, with_gap=True)
+    ds = device_stream(st)
+    sd = h2d(codes, ds.device)
+    want = torch.from_numpy(codes.view(np.int16)).cuda()
+    lib = _lib.load()
+    for lg in range(8, 15):
+        chunk = 1 << lg
+        words, _, total, offs = encode_device(sd, codes.size, book, ph.DEFAULT_LAYOUT, False, chunk)
+        assert total == st.total_bits
+        offs_h = offs.cpu().numpy().view(np.uint64)
+        # chunk c starts at the bit where symbol c*chunk starts (oracle starts)
+        lens = book.encode_arrays()[1][codes].astype(np.uint64)
+        starts = np.concatenate([[0], np.cumsum(lens)[:-1]]).astype(np.uint64)
+        assert np.array_equal(offs_h[: -(-codes.size // chunk)], starts[::chunk])
+        out = empty(codes.size, np.uint16, ds.device)
+        rep = DeviceReport(ds.device).init()
+        check(lib.bh_coarse_decode(ds.ref, offs.data_ptr(), chunk, out.data_ptr(), rep.ptr, stream_handle()),
+              "coarse")
+        check(rep.read().status, "coarse")
+        assert torch.equal(out[: codes.size], want), (key, chunk)

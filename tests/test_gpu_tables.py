@@ -1,0 +1,99 @@
+"""K1 parity: the one-launch canonical table build (bh_table_build, csrc/table.cu
+k_table_canon) against the general builder (bh_table_build_explicit: ranked
+left-justified codes plus per-entry binary search, k_fill_luts) on the same
+canonical books.  A canonical book given as explicit (code, length) pairs
+must yield byte-identical decode tables (codebook.py:86-112, :209-233)."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def env():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_09118_b200 as ph
+    from paper_2201_09118_b200 import _lib
+    return torch, ph, _lib
+
+
+def layout(max_codes: int) -> dict:
+    """Byte offsets of csrc/common.cuh TableLayout."""
+    a16 = lambda x: (x + 15) & ~15  # noqa: E731
+    L = {"lut": 64}
+    L["cnt"] = L["lut"] + 4 * 2048
+    L["dlut8"] = a16(L["cnt"] + 2 * 2048)
+    L["clut8"] = L["dlut8"] + 4 * 256
+    L["wlut8"] = a16(L["clut8"] + 256)
+    L["lut12"] = a16(L["wlut8"] + 16 * 256)
+    L["clut12"] = L["lut12"] + 4 * 4096
+    L["wlut12"] = a16(L["clut12"] + 2 * 4096)
+    L["lim"] = a16(L["wlut12"] + 16 * 4096)
+    L["base"] = L["lim"] + 8 * 33
+    L["lj"] = a16(L["base"] + 8 * 33)
+    L["ljsym"] = a16(L["lj"] + 4 * max_codes)
+    L["ljlen"] = a16(L["ljsym"] + 2 * max_codes)
+    L["total"] = a16(L["ljlen"] + max_codes)
+    return L
+
+
+def books(ph):
+    rng = np.random.default_rng(11)
+    out = [ph.canonize({0: 1}, 16), ph.canonize({0: 1, 1: 1}, 16),
+           ph.canonize({0: 1, 1: 3, 2: 3}, 8)]  # incomplete (Kraft < 1)
+    lens = {i: i + 1 for i in range(31)}
+    lens[31] = 31
+    out.append(ph.canonize(lens, 16))  # 31-bit codes
+    for bins, sigma in ((1024, 0.6), (1024, 8.0), (1024, 22.0), (4096, 0.2), (256, 3.0)):
+        codes = np.clip(np.rint(rng.normal(0, sigma, 200_000)) + bins // 2, 0, bins - 1).astype(np.uint16)
+        m = rng.random(codes.size) < 1e-3
+        codes[m] = rng.integers(0, bins, int(m.sum()))
+        out.append(ph.book_for(codes, 16))
+    for alphabet in (3000, 9000):  # alphabets beyond one 1024-symbol block / beyond 4096
+        w = 1.0 / np.arange(1, alphabet + 1)
+        syms = rng.choice(alphabet, size=300_000, p=w / w.sum()).astype(np.uint16)
+        out.append(ph.book_for(syms, 16))
+    return out
+
+
+def test_canonical_tables_match_general_builder(env):
+    torch, ph, _lib = env
+    lib = _lib.load()
+    st = torch.cuda.current_stream().cuda_stream
+    for book in books(ph):
+        max_codes = max(len(book.entries), 1)
+        L = layout(max_codes)
+        assert lib.bh_table_bytes(max_codes) == L["total"]
+        lens = book.length_bytes()
+        codes, clens = book.encode_arrays()
+        alphabet = len(lens)
+        ld = torch.from_numpy(lens.copy()).cuda()
+        cd = torch.from_numpy(codes[:alphabet].astype(np.uint32).view(np.int32).copy()).cuda()
+        cl = torch.from_numpy(clens[:alphabet].copy()).cuda()
+        fast = torch.zeros(L["total"], dtype=torch.uint8, device="cuda")
+        gen = torch.zeros(L["total"], dtype=torch.uint8, device="cuda")
+        _lib.check(lib.bh_table_build(ld.data_ptr(), alphabet, fast.data_ptr(), max_codes, st))
+        _lib.check(lib.bh_table_build_explicit(cd.data_ptr(), cl.data_ptr(), alphabet, gen.data_ptr(),
+                                               max_codes, st))
+        f, g = fast.cpu().numpy(), gen.cpu().numpy()
+        hf, hg = f[:64].view(np.uint32), g[:64].view(np.uint32)
+        assert hf[0] == 0 and hg[0] == 1          # kind: canonical / explicit
+        assert np.array_equal(hf[1:7], hg[1:7]), (hf[:7], hg[:7])  # max_len ncodes lut_bits alphabet status complete
+        ncodes = int(hf[2])
+        assert ncodes == len(book.entries)
+        for name in ("lut", "cnt", "dlut8", "clut8", "wlut8", "lut12", "clut12", "wlut12"):
+            nxt = {"lut": "cnt", "cnt": "dlut8", "dlut8": "clut8", "clut8": "wlut8", "wlut8": "lut12",
+                   "lut12": "clut12", "clut12": "wlut12", "wlut12": "lim"}[name]
+            assert np.array_equal(f[L[name]:L[nxt]], g[L[name]:L[nxt]]), (name, book.max_len, ncodes)
+        for name, w in (("lj", 4), ("ljsym", 2), ("ljlen", 1)):
+            assert np.array_equal(f[L[name]:L[name] + w * ncodes], g[L[name]:L[name] + w * ncodes]), name
+        # canonical limits (codebook.py:218-224 first_code recurrence, left-justified)
+        lim = f[L["lim"]:L["lim"] + 8 * 33].view(np.uint64)
+        counts = np.bincount(lens[lens > 0], minlength=33)
+        code = 0
+        for ln in range(1, 33):
+            assert int(lim[ln]) == (code + int(counts[ln])) << (32 - ln)
+            code = (code + int(counts[ln])) << 1

@@ -160,3 +160,17 @@ def test_chunk_stream_partitions_symbols_and_windows():
             assert b.first_entry == gap[b.sub0]
         assert ch[-1].word0 * 32 + ch[-1].total_bits == tb
         assert all(c.sub0 + c.nsub <= nsub for c in ch)
+
+
+def test_chunk_stream_rejects_unaligned_sequences():
+    """A chunk's payload pointer must stay 16-byte aligned (the fused kernel
+    stages words with 16-byte cp.async): sequences of a non-multiple of 128
+    bits, e.g. layout (32, 3, 33), cannot be chunked."""
+    import numpy as np
+    import pytest
+    from paper_2201_09118_b200 import shard
+    sb, sps = 96, 33
+    tb = sb * sps * 5
+    nsub = -(-tb // sb)
+    with pytest.raises(ValueError, match="128-bit"):
+        shard.chunk_stream(tb, sb, sps, np.zeros(nsub, np.uint8), np.ones(nsub, np.int64), 2)
