@@ -32,6 +32,8 @@ extern "C" {
 #define BH_CUDA_ERROR 8    /* CUDA runtime failure */
 #define BH_NEED_STAGED 9   /* fused path declined (incomplete codebook, or a gap entry inside a
                                   lane window that is not a codeword start); bh_decode reruns staged */
+#define BH_LENGTHOVERFLOW 10 /* LengthOverflow: an optimal code needs > 32 bits (codebook.py:76-79) */
+#define BH_EMPTY 11          /* EmptyInput: no symbol has a nonzero count (codebook.py:46-47) */
 
 #define BH_VARIANT_GAP 1     /* gap_decoder.decode (gap_decoder.py:71-92) */
 #define BH_VARIANT_SYNC 2    /* sync_decoder.decode (sync_decoder.py:173-211) */
@@ -121,6 +123,19 @@ int bh_table_build_explicit(const uint32_t *codes_dev, const uint8_t *lens_dev,
 /* canonical code per symbol (encode side); codes_dev[alphabet] */
 int bh_canonical_codes(const uint8_t *lengths_dev, uint32_t alphabet, uint32_t *codes_dev,
                        void *cuda_stream);
+
+/* ---- codebook construction on the device (codebook.py:38-83 build_lengths) */
+/* scratch for the histogram counters: u64 per symbol value */
+size_t bh_book_workspace_bytes(uint32_t alphabet);
+/* counts_dev[s] = occurrences of s among symbols_dev[0..n) (16-byte aligned) */
+int bh_symbol_histogram(const uint16_t *symbols_dev, uint64_t n, uint32_t alphabet,
+                        uint64_t *counts_dev, void *cuda_stream);
+/* Huffman code lengths identical to the reference build_lengths (ties by
+ * (count, symbol), merged subtrees after same-count leaves); lengths_dev[s] = 0
+ * for absent symbols; *status_dev = BH_OK / BH_LENGTHOVERFLOW / BH_EMPTY /
+ * BH_BAD_ARGUMENT (more than 4096 distinct symbols) */
+int bh_build_lengths(const uint64_t *counts_dev, uint32_t alphabet, uint8_t *lengths_dev,
+                     int32_t *status_dev, void *cuda_stream);
 
 /* ---- whole-decoder entry point (sync_decoder.decode / gap_decoder.decode) */
 size_t bh_workspace_bytes(const bh_stream *s, int variant, const bh_tune *tune);

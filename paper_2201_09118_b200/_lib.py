@@ -17,6 +17,7 @@ LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libb200huff.so"
 
 BH_OK, BH_INVALID, BH_TRUNCATED, BH_BADGAP, BH_NOFIXPOINT = 0, 1, 2, 3, 4
 BH_NOTPRESENT, BH_GAPOVERFLOW, BH_BAD_ARGUMENT, BH_CUDA_ERROR, BH_NEED_STAGED = 5, 6, 7, 8, 9
+BH_LENGTHOVERFLOW, BH_EMPTY = 10, 11
 VARIANT_GAP, VARIANT_SYNC, VARIANT_COARSE = 1, 2, 3
 WORD_PAD = 8
 
@@ -95,6 +96,9 @@ SIGNATURES = {
     "bh_profile_read": (I32, [C.c_char_p, SZ, P, P, I32]),
     "bh_fill_caps": (I32, [P, P, U32, P]),
     "bh_workspace_reset": (I32, [P, SZ, P]),
+    "bh_book_workspace_bytes": (SZ, [U32]),
+    "bh_symbol_histogram": (I32, [P, U64, U32, P, P]),
+    "bh_build_lengths": (I32, [P, U32, P, P, P]),
 }
 
 _lib = None
@@ -126,6 +130,8 @@ _EXC = {
     BH_NOFIXPOINT: errors.NoFixpoint,
     BH_NOTPRESENT: errors.NotPresent,
     BH_GAPOVERFLOW: errors.GapOverflow,
+    BH_LENGTHOVERFLOW: errors.LengthOverflow,
+    BH_EMPTY: errors.EmptyInput,
 }
 
 

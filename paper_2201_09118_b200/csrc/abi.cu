@@ -171,6 +171,9 @@ extern "C" const char* bh_status_string(int status) {
     case BH_GAPOVERFLOW: return "gap entry does not fit in one byte";
     case BH_BAD_ARGUMENT: return "bad argument";
     case BH_CUDA_ERROR: return "CUDA error";
+    case BH_NEED_STAGED: return "fused path declined (rerun staged)";
+    case BH_LENGTHOVERFLOW: return "optimal code needs more than 32 bits";
+    case BH_EMPTY: return "no symbol has a nonzero count";
     default: return "unknown status";
   }
 }

@@ -19,7 +19,7 @@ import numpy as np
 from . import _lib
 from ._lib import check, load, ptr, require_cuda, stream_handle
 from .bitstream import DEFAULT_LAYOUT, EncodedStream, LayoutConfig
-from .codebook import Codebook
+from .codebook import Codebook, build_lengths, canonize
 from .device import Workspace, d2h, device_stream, empty, h2d, zeros
 from .errors import GapOverflow, InvalidCode, Truncated, UnknownSymbol
 
@@ -37,6 +37,47 @@ def _words_to_units(words: np.ndarray, total_bits: int, unit_bits: int) -> np.nd
         return np.ascontiguousarray(words[:n_units], dtype=np.uint32)
     be = words.astype(">u4").view(np.uint8 if unit_bits == 8 else ">u2")
     return be[:n_units].astype(np.uint32)
+
+
+def symbol_histogram_device(symbols_dev, n: int, alphabet: int = 1 << 16):
+    """Device u64 counts per symbol value (K_hist, csrc/book.cu)."""
+    torch = require_cuda()
+    lib = load()
+    dev = symbols_dev.device
+    cells = max(int(alphabet), 8192)
+    counts = torch.empty(cells, dtype=torch.int64, device=dev)
+    src = symbols_dev
+    if src.data_ptr() % 16:
+        src = src.clone()
+    check(lib.bh_symbol_histogram(ptr(src), int(n), int(alphabet), ptr(counts), stream_handle()), "histogram")
+    return counts
+
+
+def book_for_device(symbols_dev, n: int, width: int = 16) -> Codebook:
+    """Canonical codebook fitted to a device array of uint16 symbols, built on
+    the GPU: histogram, then Huffman lengths identical to the reference
+    build_lengths (codebook.py:38-83; csrc/book.cu), then the canonical
+    numbering (codebook.py:86-112).  Up to 4096 distinct symbols on the
+    device; larger alphabets take the host build_lengths on the device
+    histogram.  An empty input gets the reference's {0: 1} book."""
+    torch = require_cuda()
+    lib = load()
+    if n == 0:
+        return canonize({0: 1}, symbol_width=width)
+    alphabet = 1 << width
+    counts = symbol_histogram_device(symbols_dev, n, alphabet)
+    lens = torch.empty(alphabet, dtype=torch.uint8, device=counts.device)
+    status = torch.zeros(1, dtype=torch.int32, device=counts.device)
+    check(lib.bh_build_lengths(ptr(counts), alphabet, ptr(lens), ptr(status), stream_handle()), "build_lengths")
+    rc = int(status.item())
+    if rc == _lib.BH_BAD_ARGUMENT:  # > 4096 distinct symbols: host heap on the device histogram
+        c = counts[:alphabet].cpu().numpy()
+        nz = np.nonzero(c)[0]
+        return canonize(build_lengths({int(s): int(c[s]) for s in nz}), symbol_width=width)
+    check(rc, "build_lengths")
+    ln = lens.cpu().numpy()
+    nz = np.nonzero(ln)[0]
+    return canonize({int(s): int(ln[s]) for s in nz}, symbol_width=width)
 
 
 def encode_device(symbols_dev, n: int, codebook: Codebook, layout: LayoutConfig = DEFAULT_LAYOUT,
