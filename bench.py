@@ -231,7 +231,7 @@ class Piece:
                                  lay.subseqs_per_seq, book.symbol_width, self.max_codes,
                                  ds.c.gap_dev + chunk.sub0, self.table.data_ptr(), chunk.first_entry, 0)
             self.n, self.tb, self.nsub, self.out0 = chunk.n, chunk.total_bits, chunk.nsub, chunk.out0
-        self.tune = make_tune(max_len=book.max_len)
+        self.tune = make_tune(max_len=book.max_len, min_len=book.min_len)
         self.tune.ctas = int(ctas)
         self.out = empty(self.n, np.uint16, ds.device)
         self.wsb = lib.bh_workspace_bytes(C.byref(self.c), self.var, C.byref(self.tune))
@@ -346,7 +346,7 @@ def e2e_measure(items, variant: str, steps: int, flush):
             self.max_codes = max(len(fs.codebook.entries), 1)
             self.args = (tb, n, lay.subseq_bits, lay.subseqs_per_seq, fs.codebook.symbol_width, fe)
             self.n = n
-            self.tune = make_tune(max_len=fs.codebook.max_len)
+            self.tune = make_tune(max_len=fs.codebook.max_len, min_len=fs.codebook.min_len)
 
     hp = [HostPiece(fs, ch) for fs, ch in items]
 

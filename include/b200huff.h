@@ -74,6 +74,8 @@ typedef struct bh_tune {
                                     shared memory (more warps per SM) */
     uint32_t ctas;               /* fused kernel CTAs (0 = one per SM): several decodes on
                                     concurrent streams can share the GPU in one wave */
+    uint32_t min_len;            /* shortest code length when known (0 = unknown); >= 4 lets
+                                    long-code books use the 8-byte three-codeword table */
 } bh_tune;
 
 /* Decode report, mirroring DecodeStats (staging.py:31-45) plus status. */
@@ -150,6 +152,15 @@ int bh_decode_async(const bh_stream *s, int variant, const bh_tune *tune, uint16
 /* zero a freshly allocated workspace once (descriptors are epoch-tagged, so
  * later calls need no reset) */
 int bh_workspace_reset(void *workspace_dev, size_t workspace_bytes, void *cuda_stream);
+/* The online tuner on the fused path (tuner.py:117-191): with tune->t_high in
+ * 1..64 the fused kernel classifies every tile by its compression ratio and
+ * stages it with that class's capacity (tuner.capacity, capacity_table
+ * overrides), and histograms the reference sequences into tuner.plan's
+ * classes.  This copies that histogram (t_high + 1 counts, n >= t_high + 1)
+ * of the last fused decode run with `ws`; BH_BAD_ARGUMENT when the layout does
+ * not put whole sequences in a tile. */
+int bh_tuner_class_freq(const bh_stream *s, const bh_tune *tune, const void *workspace_dev,
+                        uint64_t *freq_host, uint32_t n, void *cuda_stream);
 /* Synchronous convenience: decode, finish any extra seam passes, read report. */
 int bh_decode(const bh_stream *s, int variant, const bh_tune *tune, uint16_t *out_dev,
               void *workspace_dev, size_t workspace_bytes, bh_report *report_host,

@@ -41,7 +41,7 @@ class Tune(C.Structure):
     _fields_ = [
         ("t_high", U32), ("capacity", U32), ("capacity_table", U32 * 64),
         ("early_exit", U32), ("collect_stats", U32), ("fused", U32), ("seam_passes", U32),
-        ("max_len", U32), ("ctas", U32),
+        ("max_len", U32), ("ctas", U32), ("min_len", U32),
     ]
 
 
@@ -99,6 +99,7 @@ SIGNATURES = {
     "bh_book_workspace_bytes": (SZ, [U32]),
     "bh_symbol_histogram": (I32, [P, U64, U32, P, P]),
     "bh_build_lengths": (I32, [P, U32, P, P, P]),
+    "bh_tuner_class_freq": (I32, [P, P, P, P, U32, P]),
 }
 
 _lib = None

@@ -21,7 +21,7 @@ from .staging import DEFAULT_CAPACITY
 
 
 def make_tune(capacity: int = DEFAULT_CAPACITY, tuner_config=None, collect_stats: bool = False,
-              fused: bool = True, seam_passes: int = 2, max_len: int = 0) -> _lib.Tune:
+              fused: bool = True, seam_passes: int = 2, max_len: int = 0, min_len: int = 0) -> _lib.Tune:
     if capacity < 1:
         raise ValueError("staging capacity must be >= 1")
     t = _lib.Tune()
@@ -38,6 +38,7 @@ def make_tune(capacity: int = DEFAULT_CAPACITY, tuner_config=None, collect_stats
     t.fused = 1 if fused else 0
     t.seam_passes = seam_passes
     t.max_len = int(max_len)
+    t.min_len = int(min_len)
     return t
 
 
@@ -50,7 +51,8 @@ def run_decode(stream, variant: int, capacity: int = DEFAULT_CAPACITY, tuner_con
     n = int(stream.symbol_count)
     if fused is None:
         fused = stats is None
-    tune = make_tune(capacity, tuner_config, stats is not None, fused, max_len=stream.codebook.max_len)
+    tune = make_tune(capacity, tuner_config, stats is not None, fused, max_len=stream.codebook.max_len,
+                     min_len=stream.codebook.min_len)
     out = empty(n, np.uint16, ds.device)
     wsb = lib.bh_decode_workspace_bytes(ds.ref, variant, C.byref(tune))
     ws = Workspace.get(wsb, ds.device)

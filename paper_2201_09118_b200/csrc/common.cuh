@@ -62,6 +62,11 @@ struct TableHdr {
 //   lut12 u32[4096]  next 12 bits -> sym | len<<16 for codes of <= 12 bits, else 0
 //   wlut12 uint4[4096] next 12 bits -> up to 6 whole codewords, wlut8's format
 //                    (the fused kernels' decode table for long-code books)
+//   wlut12n uint2[4096] next 12 bits -> up to 3 whole codewords in 8 bytes (the
+//                    fused kernels' decode table for books whose codes are all
+//                    >= 4 bits, so no 12-bit window holds more than three):
+//                    x = s0 | s1<<16, y = s2 | len0<<16 | bits<<24 | 2n<<28
+//                    (y == 0: the first code is longer than 12 bits)
 //   clut12 u16[4096] next 12 bits -> starts | bits<<12 over every whole codeword
 //                    inside the 12 bits (count pass): bit i of `starts` is set
 //                    when a codeword starts at offset i, `bits` is where the
@@ -76,7 +81,7 @@ constexpr int FB_SIZE = 1 << FB;
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct TableLayout {
-  size_t lut, cnt, dlut8, clut8, wlut8, lut12, clut12, wlut12, lim, base, lj, ljsym, ljlen, total;
+  size_t lut, cnt, dlut8, clut8, wlut8, lut12, clut12, wlut12, wlut12n, lim, base, lj, ljsym, ljlen, total;
   __host__ __device__ explicit TableLayout(uint32_t max_codes) {
     lut = TABLE_HDR_BYTES;
     cnt = lut + sizeof(uint32_t) * LUT_SIZE;
@@ -86,7 +91,8 @@ struct TableLayout {
     lut12 = align16(wlut8 + 16 * 256);
     clut12 = lut12 + 4 * (size_t)FB_SIZE;
     wlut12 = align16(clut12 + 2 * (size_t)FB_SIZE);
-    lim = align16(wlut12 + 16 * (size_t)FB_SIZE);
+    wlut12n = align16(wlut12 + 16 * (size_t)FB_SIZE);
+    lim = align16(wlut12n + 8 * (size_t)FB_SIZE);
     base = lim + 8 * 33;
     lj = align16(base + 8 * 33);
     ljsym = align16(lj + sizeof(uint32_t) * (size_t)max_codes);

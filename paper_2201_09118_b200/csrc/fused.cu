@@ -74,6 +74,8 @@ __device__ __forceinline__ bool desc_ready(unsigned long long d, uint32_t ep) {
   return (uint32_t)(d >> 38) == (ep & EP_MASK) && (d & (3ull << 36)) != 0;
 }
 
+constexpr uint32_t TUNE_CLASSES = 65;  // classes 1..64 plus the overflow group (t_high <= 64 on this path)
+
 struct FusedArgs {
   const uint32_t* words;
   uint64_t words_alloc;  // readable words (payload + pad), multiple of 4
@@ -105,6 +107,15 @@ struct FusedArgs {
   uint32_t t_lim, t_c12, t_wp, t_l12;  // shared-memory table offsets (bytes)
   uint32_t t_ljs, ljs_bytes;            // shared copy of ljsym for the limit search (0 bytes: global)
   uint32_t smem_tiles;                  // ranges up to this many tiles keep their totals in shared memory
+  // online tuner (tuner.py:117-191): 0 = off; else per-tile class -> staging
+  // window, and the per-sequence class histogram of tuner.plan
+  uint32_t t_high;
+  uint32_t lanes_per_seq;               // lanes per reference sequence (0: the histogram is not exported)
+  uint32_t sym_w;                       // Codebook.symbol_width
+  uint32_t ref_seq_bits;                // LayoutConfig.seq_bits
+  uint64_t nseq_ref;                    // reference sequences
+  unsigned long long* class_freq;       // [t_high + 1] (zeroed before the launch)
+  uint32_t cls_cap[TUNE_CLASSES];       // staging capacity per 1-based class (tuner.capacity)
   unsigned long long* trace;  // debug timeline (TR instantiation only)
 };
 
@@ -122,6 +133,14 @@ constexpr unsigned long long FUSED_MARK = 0xF05EDull;  // rep->pad[2]: report wr
 constexpr uint32_t T_LIMBASE = 2 * 33 * 8;  // lim u64[33], base i64[33] (contiguous)
 constexpr uint32_t T_NARROW_DEC = 256 * 8 * 16;
 constexpr uint32_t T_WIDE_DEC = 16 * FB_SIZE;
+constexpr uint32_t T_WIDE3_DEC = 8 * FB_SIZE;
+// Decode-table modes (template parameter MODE of the kernel):
+//   M_NARROW -- 8-bit window, up to six codewords, 16-byte entries replicated 8 ways;
+//   M_WIDE   -- 12-bit window, up to six codewords, 16-byte entries (wlut12);
+//   M_WIDE3  -- 12-bit window, up to three codewords, 8-byte entries (wlut12n),
+//               for books whose codes are all >= 4 bits: half the table, half
+//               the shared-memory wavefronts per lookup and no store predicates.
+constexpr int M_NARROW = 0, M_WIDE = 1, M_WIDE3 = 2;
 
 // rep->pad[3] = epoch: the fused path declined this call (overrides every
 // status; bh_decode reruns the reference-structured pipeline)
@@ -266,8 +285,14 @@ __device__ __forceinline__ uint32_t flong(uint32_t win, const FTab& T) {
 }
 
 // one codeword: sym | len<<16 (0 = no codeword matches)
+template <int MODE>
 __device__ __forceinline__ uint32_t fone(uint32_t win, const FTab& T) {
-  const uint4 w = lds128(T.wl + ((win >> T.dsh) << T.dst));
+  if (MODE == M_WIDE3) {
+    const uint2 e = lds64(T.wl + ((win >> (32 - FB)) << 3));
+    if (e.y) return (e.x & 0xffffu) | (((e.y >> 16) & 31u) << 16);
+    return flong(win, T);
+  }
+  const uint4 w = lds128(T.wl + (MODE == M_WIDE ? (win >> (32 - FB)) << 4 : (win >> 24) << 7));
   if (w.w) return (w.x & 0xffffu) | (((w.w >> 16) & 15u) << 16);
   return flong(win, T);
 }
@@ -329,8 +354,59 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
 // (the ones past the entry's count land inside the lane's own range and are
 // overwritten by its next stores); the last entries store predicated, so lane
 // ranges stay disjoint even for corrupt (non-contiguous) windows.
+// Three-codeword entries (M_WIDE3): per lookup one halfword store and two word
+// stores, unconditionally -- an even start writes s0|s1 and s2 (plus junk in
+// the high half), an odd start s0 then s1|s2 (plus a junk word) -- at most 10
+// bytes, all inside the lane's remaining range while >= 10 bytes remain, and
+// overwritten by its next stores.
+__device__ __forceinline__ bool fdecode3(SR& r, uint32_t c, uint32_t dst, const FTab& T) {
+  const uint32_t wl = pin(T.wl);
+  int32_t k2 = 2 * (int32_t)c;  // remaining staging bytes
+  while (k2 > 0) {
+#pragma unroll (kUnroll)
+    while (k2 >= 10) {
+      const uint2 e = lds64(wl + ((r.peek() >> (32 - FB)) << 3));
+      if (!e.y) break;  // a code longer than 12 bits: one codeword below
+      const uint32_t odd = dst & 2u;
+      const uint32_t a4 = dst + odd;
+      sts16(dst, e.x);
+      sts32(a4, __funnelshift_r(e.x, e.y, odd << 3));  // even: s0|s1, odd: s1|s2
+      sts32(a4 + 4, e.y);                              // even: s2 (+ junk), odd: junk
+      const uint32_t nb = e.y >> 28;                   // 2n: bytes of staging written
+      dst += nb;
+      k2 -= (int32_t)nb;
+      r.skip((e.y >> 24) & 15u);
+    }
+    if (k2 <= 0) break;
+    const uint32_t win = r.peek();
+    const uint2 e = lds64(wl + ((win >> (32 - FB)) << 3));
+    if (e.y) {
+      const int32_t n = (int32_t)(e.y >> 29), k = k2 >> 1;
+      const int32_t m = n < k ? n : k;
+      sts16(dst, e.x);
+      if (m > 1) sts16(dst + 2, e.x >> 16);
+      if (m > 2) sts16(dst + 4, e.y);
+      dst += (uint32_t)n << 1;
+      k2 -= 2 * n;
+      r.skip((e.y >> 24) & 15u);
+    } else {
+      const uint32_t el = flong(win, T);
+      const uint32_t len = (el >> 16) & 0xffu;
+      if (!len) return false;
+      sts16(dst, el);
+      dst += 2;
+      k2 -= 2;
+      r.skip(len);
+    }
+  }
+  return true;
+}
+
+template <int MODE>
 __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const FTab& T) {
-  const uint32_t wl = pin(T.wl), dsh = T.dsh, dstr = T.dst;
+  if (MODE == M_WIDE3) return fdecode3(r, c, dst, T);
+  constexpr uint32_t dsh = MODE == M_WIDE ? 32 - FB : 24, dstr = MODE == M_WIDE ? 4 : 7;
+  const uint32_t wl = pin(T.wl);
   int32_t k = (int32_t)c;
   while (k > 0) {
     // tight loop: whole entries while at least seven symbols remain; one
@@ -387,9 +463,10 @@ __device__ __forceinline__ bool fdecode(SR& r, uint32_t c, uint32_t dst, const F
 }
 
 // bypass: decode straight to global memory (rare; guarded by the output size)
+template <int MODE>
 __device__ bool fdecode_global(SR& r, uint32_t c, uint16_t* out, uint64_t at, uint64_t nsym, const FTab& T) {
   for (uint32_t k = 0; k < c; ++k) {
-    const uint32_t s = fone(r.peek(), T);
+    const uint32_t s = fone<MODE>(r.peek(), T);
     const uint32_t len = (s >> 16) & 0xffu;
     if (!len) return false;
     if (at + k < nsym) out[at + k] = (uint16_t)s;
@@ -432,11 +509,12 @@ __device__ __forceinline__ bool resync_step(uint32_t base_s, uint32_t eo, uint32
   }
 }
 
+template <int MODE>
 __device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co, uint32_t xo, uint32_t en,
                                        uint32_t stop, const FTab& T, uint32_t& cn, uint32_t& xn) {
-  // long-code books (wide layout): a 12-bit entry holds a codeword or two, so
+  // long-code books (wide layouts): a 12-bit entry holds a codeword or two, so
   // the plain per-codeword walk is cheaper there
-  if (T.dsh != 24) return resync_step(base_s, eo, co, xo, en, stop, T, cn, xn);
+  if (MODE != M_NARROW) return resync_step(base_s, eo, co, xo, en, stop, T, cn, xn);
   uint32_t po = eo, pn = en, no = 0, nn = 0;
   SR ro, rn;
   ro.init(base_s, po);
@@ -686,7 +764,7 @@ __device__ __forceinline__ void flush_aligned(uint16_t* __restrict__ out, uint64
 // tile publishes its exit when no candidate changes it (else a DEP marker);
 // seed_o >= 0 -- the true seed offset is known: the final state is computed
 // and the exit published.
-template <int VAR>
+template <int VAR, int MODE>
 __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, uint64_t tile, uint32_t base_s,
                                             uint64_t wb0, uint32_t nsl, uint32_t ep, uint32_t& e, uint32_t& c,
                                             bool& bad, int32_t seed_o = -1, uint32_t* cand_out = nullptr,
@@ -749,7 +827,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
       bool dnow = false;
       if (live && xin != e) {
         uint32_t cn, xn;
-        if (!resync(base_s, e, c, x, xin, stop, T, cn, xn)) bad = true;
+        if (!resync<MODE>(base_s, e, c, x, xin, stop, T, cn, xn)) bad = true;
         e = xin;
         c = cn;
         x = xn;
@@ -768,7 +846,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
       // only offsets below the longest code length are candidates
 #ifndef BH_X_NOCAND
       if (lane < T.max_len) {
-        if (!resync(base_s, b0, c0, x0, b0 + lane, stop0, T, cand_c, cand_x)) cand_x = 0xffffffffu;
+        if (!resync<MODE>(base_s, b0, c0, x0, b0 + lane, stop0, T, cand_c, cand_x)) cand_x = 0xffffffffu;
       }
 #endif
       indep = __all_sync(0xffffffffu, cand_x == x0);
@@ -785,7 +863,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
         const uint32_t ek = __shfl_sync(0xffffffffu, e, k), ck = __shfl_sync(0xffffffffu, c, k);
         const uint32_t xk = __shfl_sync(0xffffffffu, x, k), sk = __shfl_sync(0xffffffffu, stop, k);
         uint32_t cn, xn;
-        if (cx == 0xffffffffu || !resync(base_s, ek, ck, xk, cx, sk, T, cn, xn)) xn = 0xffffffffu;
+        if (cx == 0xffffffffu || !resync<MODE>(base_s, ek, ck, xk, cx, sk, T, cn, xn)) xn = 0xffffffffu;
         cx = xn;
         if (__all_sync(0xffffffffu, cx == xk)) {
           indep = true;
@@ -816,7 +894,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
           bool dnow = false;
           if (live && xin != e) {
             uint32_t cn, xn;
-            if (!resync(base_s, e, c, x, xin, stop, T, cn, xn)) bad = true;
+            if (!resync<MODE>(base_s, e, c, x, xin, stop, T, cn, xn)) bad = true;
             e = xin;
             c = cn;
             x = xn;
@@ -928,7 +1006,7 @@ __device__ unsigned long long lookback_wide(unsigned long long* desc, uint64_t c
 constexpr uint32_t MAX_SMEM_TILES = 512;
 constexpr int32_t FULL_FIX = 0x7fffffff;  // tile_dlt marker: re-synchronise the whole tile in the fix-up
 
-template <int VAR, int TR>
+template <int VAR, int TR, int MODE>
 __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a) {
 #define MARK(slot)                                                                                  \
   do {                                                                                              \
@@ -945,6 +1023,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   __shared__ uint32_t s_carry;
   __shared__ uint32_t s_next;  // phase 2: next tile of the range to take
   __shared__ unsigned long long s_tcount, s_tseam;  // phase clocks (count loop end, seam fix-up end)
+  __shared__ uint32_t s_cls[TUNE_CLASSES];           // tuner: sequences per class
   __shared__ uint32_t s_tcnt[MAX_SMEM_TILES];  // symbols per tile of the range (short ranges)
   // SYNC, short ranges: the range's exit descriptors and full-fix flags, so
   // the seam fix-up reads in-range predecessors from shared memory
@@ -986,7 +1065,10 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     bulk_g2s(sm_s + a.t_c12, tb_ + L.clut12, 2 * FB_SIZE, bar_ct);
     if (a.ljs_bytes) bulk_g2s(sm_s + a.t_ljs, tb_ + L.ljsym, a.ljs_bytes, bar_ct);
     bulk_g2s(sm_s + a.t_lim, tb_ + L.lim, T_LIMBASE, bar_ct);  // lim, base (contiguous)
-    if (a.wide) {
+    if (MODE == M_WIDE3) {
+      mbar_expect_tx(bar_dt, T_WIDE3_DEC);
+      bulk_g2s(sm_s, tb_ + L.wlut12n, T_WIDE3_DEC, bar_dt);
+    } else if (MODE == M_WIDE) {
       mbar_expect_tx(bar_dt, T_WIDE_DEC);
       bulk_g2s(sm_s, tb_ + L.wlut12, T_WIDE_DEC, bar_dt);
     } else {
@@ -1007,12 +1089,12 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   if (tile < t1) wb_a = stage_words(a, tile, land, nch_a);
   cp_commit();
   FTab T;
-  T.wl = a.wide ? sm_s : sm_s + 16 * (lane & 7);
-  T.dsh = a.wide ? 32 - FB : 24;
-  T.dst = a.wide ? 4 : 7;
+  T.wl = MODE != M_NARROW ? sm_s : sm_s + 16 * (lane & 7);
+  T.dsh = MODE != M_NARROW ? 32 - FB : 24;
+  T.dst = MODE == M_WIDE3 ? 3 : MODE == M_WIDE ? 4 : 7;
   T.lim = sm_s + a.t_lim;
   T.base = sm_s + a.t_lim + 33 * 8;
-  T.l12 = (!a.wide && a.has_l12) ? sm_s + a.t_l12 : 0u;
+  T.l12 = (MODE == M_NARROW && a.has_l12) ? sm_s + a.t_l12 : 0u;
   T.c12 = sm_s + a.t_c12;
   T.ljs = (a.ljs_bytes && hdr->kind == 0) ? sm_s + a.t_ljs : 0u;
   T.t = table_view(a.table, a.max_codes, hdr->ncodes);
@@ -1020,6 +1102,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   T.max_len = hdr->max_len ? min(hdr->max_len, 32u) : 32u;
   if (VAR == BH_VARIANT_SYNC)
     for (uint32_t i = threadIdx.x; i < SX; i += blockDim.x) { s_texit[i] = 0; s_tff[i] = 0; }
+  for (uint32_t i = threadIdx.x; i < TUNE_CLASSES; i += blockDim.x) s_cls[i] = 0;
   if (threadIdx.x == 0) {
     s_next = W;  // phase 2 starts with tile t0 + warp index
     s_tcount = s_tseam = 0;
@@ -1062,7 +1145,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     uint32_t e, c, cand = 0;
     bool fullfix = false;
     unsigned long long dsc = 0;
-    tile_counts<VAR>(a, T, tile, dbuf_s, wb_a, nsl, ep, e, c, bad, -1, &cand, &fullfix,
+    tile_counts<VAR, MODE>(a, T, tile, dbuf_s, wb_a, nsl, ep, e, c, bad, -1, &cand, &fullfix,
                      VAR == BH_VARIANT_GAP && a.sps == 32 ? gcur : nullptr, &dsc);
     if (kidx < 8) MARK(11 + 2 * kidx);
     gcur[0] = gnext[0];
@@ -1193,7 +1276,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - st * a.sps);
         uint32_t e, c;
         unsigned long long dsc = 0;
-        tile_counts<VAR>(a, T, st, dbuf_s, wbs, nsl, ep, e, c, bad, (int32_t)min(o, 255u), nullptr, nullptr,
+        tile_counts<VAR, MODE>(a, T, st, dbuf_s, wbs, nsl, ep, e, c, bad, (int32_t)min(o, 255u), nullptr, nullptr,
                          nullptr, &dsc);
         if (lane == 0 && srange) *(volatile unsigned long long*)&s_texit[st - t0] = dsc;
         uint32_t incl = c;
@@ -1220,7 +1303,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   // ---- tile offsets within the range, CTA aggregate -----------------------
   // wlut8 replicated 8 ways ([entry][replica] uint4) from its packed copy
   mbar_wait(bar_dt, 0);
-  if (!a.wide)
+  if (MODE == M_NARROW)
     for (uint32_t i = threadIdx.x; i < 256 * 8; i += blockDim.x)
       sts128(sm_s + 16 * i, lds128(sm_s + a.t_wp + 16 * (i >> 3)));
   __syncthreads();  // tile totals and the replicated decode table visible
@@ -1351,7 +1434,34 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       have_off = __shfl_sync(0xffffffffu, lane == 0 ? mbar_test(bar_off, 0) : 0u, 0) != 0;
       if (have_off) Pc = *(volatile unsigned long long*)&s_ctaoff;
     }
-    const bool fits = C + 16 <= a.cap;
+    bool fits = C + 16 <= a.cap;
+    uint32_t capw = a.cap - 8;  // staging window of the reference rounds (staging.py:123-146)
+    if (a.t_high) {
+      // online tuner (tuner.py:117-191, PAPER Alg. 2): the tile's class from its
+      // own compression ratio sets its staging capacity (tuner.capacity); a
+      // tile above it takes the reference's rounds with that capacity
+      const uint64_t tbits = min((uint64_t)a.seq_bits, a.tb - tile * (uint64_t)a.seq_bits);
+      const uint32_t tcls =
+          C ? (uint32_t)min(((uint64_t)C * a.sym_w + tbits - 1) / tbits, (uint64_t)a.t_high + 1) : 1u;
+      const uint32_t cc = a.cls_cap[tcls - 1];
+      if (cc < capw) capw = cc;
+      if (C > cc) fits = false;
+      if (a.lanes_per_seq) {
+        // tuner.plan's classes of the reference sequences this tile holds
+        // (tuner.py:126-133: ceil(count * width / bits), the last sequence's
+        // actual bits, an empty sequence in class 1)
+        uint32_t v = c;
+        for (uint32_t sw = 1; sw < a.lanes_per_seq; sw <<= 1) v += __shfl_xor_sync(0xffffffffu, v, sw);
+        if (lane % a.lanes_per_seq == 0) {
+          const uint64_t q = tile * (uint64_t)(32 / a.lanes_per_seq) + lane / a.lanes_per_seq;
+          if (q < a.nseq_ref) {
+            const uint64_t qb = q + 1 < a.nseq_ref ? (uint64_t)a.ref_seq_bits : a.tb - q * (uint64_t)a.ref_seq_bits;
+            const uint32_t k = v ? (uint32_t)min(((uint64_t)v * a.sym_w + qb - 1) / qb, (uint64_t)a.t_high + 1) : 1u;
+            atomicAdd(&s_cls[k - 1], 1u);
+          }
+        }
+      }
+    }
     const uint32_t sh = have_off ? (uint32_t)(Pc + toff) & 7u : 0u;
     if (bulk_pending) {  // the previous tile's bulk copy must have read the staging
       if (lane == 0) bulk_read_wait();
@@ -1361,7 +1471,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     if (fits && c) {
       SR r;
       r.init(base_s, e);
-      if (!fdecode(r, c, stg_s + 2 * (sh + o), T)) bad = true;
+      if (!fdecode<MODE>(r, c, stg_s + 2 * (sh + o), T)) bad = true;
     }
     __syncwarp();
     if (dk < 8) MARK(31 + 3 * dk);
@@ -1380,7 +1490,6 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     } else {
       // reference rounds (staging.py:123-146) with capacity cap - 8
       const bool active = lane < nsl;
-      const uint32_t capw = a.cap - 8;
       const uint32_t endl = o + c;
       uint32_t si = 0;
       while (si < C) {
@@ -1393,7 +1502,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
           if (lane == jl) {
             SR r;
             r.init(base_s, e);
-            if (!fdecode_global(r, c, a.out, P + o, a.nsym, T)) bad = true;
+            if (!fdecode_global<MODE>(r, c, a.out, P + o, a.nsym, T)) bad = true;
           }
           si = __shfl_sync(0xffffffffu, endl, jl);
           continue;
@@ -1406,7 +1515,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
             if (mine) {
           SR r;
           r.init(base_s, e);
-          if (!fdecode(r, c, d, T)) bad = true;
+          if (!fdecode<MODE>(r, c, d, T)) bad = true;
         }
         __syncwarp();
 
@@ -1426,6 +1535,11 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging read (writes land by kernel end)
   if (!have_off) mbar_wait(bar_off, 0);  // keep warp 0's arrival inside the CTA's lifetime
   if (__any_sync(0xffffffffu, bad) && lane == 0) tag_status(a.rep, ep, BH_INVALID);
+  if (a.t_high && a.lanes_per_seq) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i <= a.t_high; i += blockDim.x)
+      if (s_cls[i]) atomicAdd(&a.class_freq[i], (unsigned long long)s_cls[i]);
+  }
   MARK(TRACE_SLOTS - 2);
   fused_finish(a, ep);
   MARK(TRACE_SLOTS - 1);
@@ -1472,7 +1586,7 @@ inline uint64_t nseq_of(const bh_stream* s) { return (vnsub_of(s) + TILE_SUBSEQ 
 
 
 struct FusedCfg {
-  uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12, wide, t_lim, t_c12, t_wp, t_l12, t_ljs, ljs_bytes;
+  uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12, wide, mode, t_lim, t_c12, t_wp, t_l12, t_ljs, ljs_bytes;
 };
 
 FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
@@ -1498,8 +1612,13 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   // symbols out of the conflict-free 8-bit one)
   c.wide = c.has_l12 && 2 * s->total_bits > 3 * s->symbol_count;
   if (env_int("BH_FUSED_WIDE", -1) >= 0) c.wide = env_int("BH_FUSED_WIDE", 0) != 0;
+  // books whose codes are all >= 4 bits never put more than three codewords in
+  // a 12-bit window: the 8-byte three-codeword table then decodes the same
+  c.mode = !c.wide ? M_NARROW : (tune && tune->min_len >= 4 ? M_WIDE3 : M_WIDE);
+  if (c.wide && env_int("BH_FUSED_MODE", -1) >= 1) c.mode = env_int("BH_FUSED_MODE", 1) == 2 && tune &&
+                                                                     tune->min_len >= 4 ? M_WIDE3 : M_WIDE;
   if (c.wide) {
-    c.t_lim = T_WIDE_DEC;
+    c.t_lim = c.mode == M_WIDE3 ? T_WIDE3_DEC : T_WIDE_DEC;
     c.t_c12 = c.t_lim + T_LIMBASE;
     c.t_wp = c.t_l12 = 0;
     c.tables = (uint32_t)align16(c.t_c12 + 2 * FB_SIZE);
@@ -1547,10 +1666,13 @@ extern "C" int bh_debug_fused_trace(void* trace_dev) {
   return BH_OK;
 }
 
-extern "C" int bh_debug_fused_shape(const bh_stream* s, const bh_tune* tune, uint32_t* warps, uint32_t* smem) {
+extern "C" int bh_debug_fused_shape(const bh_stream* s, const bh_tune* tune, uint32_t* warps, uint32_t* smem,
+                                    uint32_t* cap, uint32_t* spl) {
   FusedCfg c = fused_cfg(s, tune);
   if (warps) *warps = c.warps;
   if (smem) *smem = c.smem;
+  if (cap) *cap = c.cap;
+  if (spl) *spl = spl_of(s);
   return BH_OK;
 }
 
@@ -1570,8 +1692,36 @@ extern "C" int bh_fused_supported(const bh_stream* s, int variant) {
 // workspace: [64 B header: epoch, CTA-done counter][cnt desc][exit desc]
 //            [lane info u32 x 32 per tile][tile count u32][tile offset u32]
 //            [seed candidates u16 x 32 per tile][first-slot delta i32]
+static size_t class_freq_offset(const bh_stream* s) {
+  return 64 + 16 * nseq_of(s) + 4 * 34 * nseq_of(s) + 64 * nseq_of(s) + 4 * nseq_of(s);
+}
+
 extern "C" size_t bh_fused_workspace_bytes(const bh_stream* s, int, const bh_tune*) {
-  return 64 + 16 * nseq_of(s) + 4 * 34 * nseq_of(s) + 64 * nseq_of(s) + 4 * nseq_of(s) + 256;
+  return align16(class_freq_offset(s)) + 8 * TUNE_CLASSES + 256;
+}
+
+// Which lanes form one reference sequence (tile = 32 lanes of spl subsequences):
+// the per-sequence histogram needs whole sequences per tile.
+static uint32_t lanes_per_seq_of(const bh_stream* s) {
+  const uint32_t spl = spl_of(s), sps = s->subseqs_per_seq;
+  if (sps % spl) return 0;
+  const uint32_t l = sps / spl;
+  return (l && l <= 32 && 32 % l == 0) ? l : 0;
+}
+
+static bool tuned(const bh_tune* t) { return t && t->t_high && t->t_high < TUNE_CLASSES; }
+
+// tuner.plan's class histogram of the last fused decode with this workspace
+// (stream-ordered copy, then a sync): freq_host[0..t_high]
+extern "C" int bh_tuner_class_freq(const bh_stream* s, const bh_tune* tune, const void* ws, uint64_t* freq_host,
+                                   uint32_t n, void* cuda_stream) {
+  if (!s || !ws || !freq_host || !tuned(tune) || n < tune->t_high + 1) return BH_BAD_ARGUMENT;
+  if (!lanes_per_seq_of(s)) return BH_BAD_ARGUMENT;
+  const char* p = static_cast<const char*>(ws) + align16(class_freq_offset(s));
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  if (cudaMemcpyAsync(freq_host, p, 8 * (size_t)(tune->t_high + 1), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return BH_CUDA_ERROR;
+  return cudaStreamSynchronize(st) == cudaSuccess ? BH_OK : BH_CUDA_ERROR;
 }
 
 extern "C" int bh_workspace_reset(void* ws, size_t bytes, void* cuda_stream) {
@@ -1624,13 +1774,39 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.t_l12 = cfg.t_l12;
   a.t_ljs = cfg.t_ljs;
   a.ljs_bytes = cfg.ljs_bytes;
+  a.t_high = 0;
+  a.lanes_per_seq = 0;
+  if (tuned(tune)) {
+    // capacities per class (tuner.py:98-106 with capacity_table overrides)
+    a.t_high = tune->t_high;
+    for (uint32_t c = 1; c <= a.t_high + 1; ++c) {
+      uint32_t v = c <= 64 && tune->capacity_table[c - 1] ? tune->capacity_table[c - 1]
+                                                          : (c > a.t_high ? 3584u : c * 1024u);
+      a.cls_cap[c - 1] = v ? v : 1u;
+    }
+    a.lanes_per_seq = lanes_per_seq_of(s);
+    a.sym_w = s->symbol_width ? s->symbol_width : 16u;
+    a.ref_seq_bits = s->subseq_bits * s->subseqs_per_seq;
+    a.nseq_ref = (nsub_of(s) + s->subseqs_per_seq - 1) / s->subseqs_per_seq;
+    a.class_freq = reinterpret_cast<unsigned long long*>(static_cast<char*>(ws) + align16(class_freq_offset(s)));
+    if (cudaMemsetAsync(a.class_freq, 0, 8 * (size_t)(a.t_high + 1), static_cast<cudaStream_t>(cuda_stream)) !=
+        cudaSuccess)
+      return BH_CUDA_ERROR;
+  }
   a.smem_tiles = (uint32_t)env_int("BH_FUSED_SMEM_TILES", (int)MAX_SMEM_TILES);
   if (a.smem_tiles > MAX_SMEM_TILES) a.smem_tiles = MAX_SMEM_TILES;
   const int sms = device_sm_count();
   a.trace = g_trace.load(std::memory_order_relaxed);
-  const void* fn =
-      variant == BH_VARIANT_GAP ? (a.trace ? (const void*)k_fused2<BH_VARIANT_GAP, 1> : (const void*)k_fused2<BH_VARIANT_GAP, 0>)
-                                : (a.trace ? (const void*)k_fused2<BH_VARIANT_SYNC, 1> : (const void*)k_fused2<BH_VARIANT_SYNC, 0>);
+  static const void* const kern[2][2][3] = {
+      {{(const void*)k_fused2<BH_VARIANT_GAP, 0, M_NARROW>, (const void*)k_fused2<BH_VARIANT_GAP, 0, M_WIDE>,
+        (const void*)k_fused2<BH_VARIANT_GAP, 0, M_WIDE3>},
+       {(const void*)k_fused2<BH_VARIANT_GAP, 1, M_NARROW>, (const void*)k_fused2<BH_VARIANT_GAP, 1, M_WIDE>,
+        (const void*)k_fused2<BH_VARIANT_GAP, 1, M_WIDE3>}},
+      {{(const void*)k_fused2<BH_VARIANT_SYNC, 0, M_NARROW>, (const void*)k_fused2<BH_VARIANT_SYNC, 0, M_WIDE>,
+        (const void*)k_fused2<BH_VARIANT_SYNC, 0, M_WIDE3>},
+       {(const void*)k_fused2<BH_VARIANT_SYNC, 1, M_NARROW>, (const void*)k_fused2<BH_VARIANT_SYNC, 1, M_WIDE>,
+        (const void*)k_fused2<BH_VARIANT_SYNC, 1, M_WIDE3>}}};
+  const void* fn = kern[variant == BH_VARIANT_GAP ? 0 : 1][a.trace ? 1 : 0][cfg.mode];
   // launch attributes and occupancy cached per (device, kernel, threads,
   // smem): the dynamic shared-memory opt-in is a per-device (per-context)
   // function attribute

@@ -172,6 +172,27 @@ __global__ void k_explicit_hdr(const uint8_t* __restrict__ lens, uint32_t alphab
   }
 }
 
+// 8-byte entry of up to three whole codewords of the 12-bit window v (wlut12n)
+__device__ __forceinline__ uint2 pack3(uint32_t s0, uint32_t s1, uint32_t s2, uint32_t n3, uint32_t l0, uint32_t p3) {
+  uint2 e;
+  e.x = s0 | (s1 << 16);
+  e.y = n3 ? (s2 | (l0 << 16) | (p3 << 24) | ((2 * n3) << 28)) : 0u;
+  return e;
+}
+
+__device__ __forceinline__ uint2 narrow3(uint32_t a, uint32_t b, uint32_t c, int v, const uint32_t* s_l12) {
+  uint32_t p = 0, n = 0, l0 = 0;
+  while (n < 3 && p < (uint32_t)FB) {
+    const uint32_t f = s_l12[((uint32_t)v << p) & (FB_SIZE - 1)];
+    const uint32_t len = (f >> 16) & 0xff;
+    if (len == 0 || p + len > (uint32_t)FB) break;
+    if (n == 0) l0 = len;
+    p += len;
+    ++n;
+  }
+  return pack3(n > 0 ? a : 0u, n > 1 ? b : 0u, n > 2 ? c : 0u, n, l0, p);
+}
+
 // First-level tables from the sorted long-code arrays (one CTA).
 __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_codes) {
   TableHdr* hdr; uint32_t* lut; uint16_t* cnt; uint32_t* lj; uint16_t* ljsym; uint8_t* ljlen;
@@ -216,6 +237,7 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
   __syncthreads();
   // up to six whole codewords of the 12-bit window (wide decode table)
   uint4* wlut12 = reinterpret_cast<uint4*>(reinterpret_cast<char*>(blob) + L.wlut12);
+  uint2* wlut12n = reinterpret_cast<uint2*>(reinterpret_cast<char*>(blob) + L.wlut12n);
   for (int v = threadIdx.x; v < FB_SIZE; v += blockDim.x) {
     uint32_t p6 = 0, n6 = 0, sy[6] = {0, 0, 0, 0, 0, 0}, l0 = 0;
     while (n6 < 6 && p6 < (uint32_t)FB) {
@@ -232,6 +254,7 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
     wl.z = sy[4] | (sy[5] << 16);
     wl.w = n6 ? (p6 | (n6 << 4) | (l0 << 16) | ((2 * n6) << 28)) : 0u;
     wlut12[v] = wl;
+    wlut12n[v] = narrow3(sy[0], sy[1], sy[2], v, s_l12);
   }
   uint16_t* s_len12 = reinterpret_cast<uint16_t*>(s_lut);  // 4096 lengths (8 KB)
   for (int v = threadIdx.x; v < FB_SIZE; v += blockDim.x) s_len12[v] = (uint16_t)((s_l12[v] >> 16) & 0xff);
@@ -291,8 +314,8 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
 // limit exceeds the window, a 5-step search over 33 shared values) and its
 // symbol by base[len] + code -- no per-entry global binary search.
 // ---------------------------------------------------------------------------
-constexpr int K1_THREADS = 512;
-constexpr int K1_GRID = 16;
+constexpr int K1_THREADS = 1024;  // 32 warps: one per code length in the rank scan
+constexpr int K1_GRID = 8;
 
 struct CanonSmem {
   unsigned long long lim[33];
@@ -300,6 +323,7 @@ struct CanonSmem {
   uint32_t count[33];
   uint32_t fill[33];
   uint32_t wcnt[K1_THREADS / 32][33];
+  uint32_t wpre[K1_THREADS / 32][33];
   uint16_t sym[FB_SIZE];  // canonical order of the codes of length <= 12
   int bad;
 };
@@ -340,41 +364,61 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
     else if (ln) atomicAdd(&S.count[ln], 1u);
   }
   __syncthreads();
-  if (tid == 0) {
-    unsigned long long code = 0, kraft = 0;
-    uint32_t idx = 0, ml = 0;
-    S.lim[0] = 0;
-    S.base[0] = 0;
-#pragma unroll 1
-    for (int ln = 1; ln <= 32; ++ln) {
-      const uint32_t c = S.count[ln];
-      S.lim[ln] = (code + c) << (32 - ln);
-      S.base[ln] = (long long)idx - (long long)code;
-      S.fill[ln] = idx;  // first_index: rank base of the length
-      code = (code + c) << 1;
-      idx += c;
-      kraft += (unsigned long long)c << (32 - ln);
-      if (c) ml = ln;
+  // first_code / first_index per length (codebook.py:209-233) as one warp scan:
+  // lane ln-1 holds count c and its left-justified Kraft share d = c << (32-ln);
+  // the exclusive prefix of d is first_code << (32-ln) exactly, and its
+  // inclusive prefix the canonical limit lim[ln] = (first_code + c) << (32-ln)
+  if (warp == 0) {
+    const uint32_t ln = lane + 1;
+    const uint32_t c = S.count[ln];
+    const unsigned long long d = (unsigned long long)c << (32 - ln);
+    unsigned long long P = d;
+    uint32_t I = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned long long y = __shfl_up_sync(0xffffffffu, P, o);
+      const uint32_t z = __shfl_up_sync(0xffffffffu, I, o);
+      if (lane >= o) { P += y; I += z; }
     }
-    if (idx > max_codes) S.bad = 1;
+    const unsigned long long code = (P - d) >> (32 - ln);
+    S.lim[ln] = P;
+    S.base[ln] = (long long)(I - c) - (long long)code;
+    S.fill[ln] = I - c;  // first_index: rank base of the length
+    const uint32_t ncodes = __shfl_sync(0xffffffffu, I, 31);
+    const unsigned long long kraft = __shfl_sync(0xffffffffu, P, 31);
+    const unsigned used = __ballot_sync(0xffffffffu, c != 0);
+    const uint32_t ml = used ? 32 - __clz(used) : 0;
+    if (lane == 0) {
+      S.lim[0] = 0;
+      S.base[0] = 0;
+      if (ncodes > max_codes) S.bad = 1;
+    }
+    __syncwarp();
     if (cta == 0) {
-      hdr->kind = 0;
-      hdr->max_len = ml;
-      hdr->ncodes = idx;
-      hdr->lut_bits = LUT_BITS;
-      hdr->alphabet = alphabet;
-      hdr->status = S.bad ? BH_BAD_ARGUMENT : BH_OK;
-      hdr->complete = kraft == (1ull << 32) ? 1u : 0u;
       TableLayout L(max_codes);
       unsigned long long* glim = reinterpret_cast<unsigned long long*>(reinterpret_cast<char*>(blob) + L.lim);
       long long* gbase = reinterpret_cast<long long*>(reinterpret_cast<char*>(blob) + L.base);
-#pragma unroll 1
-      for (int ln = 0; ln <= 32; ++ln) { glim[ln] = S.lim[ln]; gbase[ln] = S.base[ln]; }
+      glim[ln] = P;
+      gbase[ln] = S.base[ln];
+      if (lane == 0) {
+        glim[0] = 0;
+        gbase[0] = 0;
+        hdr->kind = 0;
+        hdr->max_len = ml;
+        hdr->ncodes = ncodes;
+        hdr->lut_bits = LUT_BITS;
+        hdr->alphabet = alphabet;
+        hdr->status = S.bad ? BH_BAD_ARGUMENT : BH_OK;
+        hdr->complete = kraft == (1ull << 32) ? 1u : 0u;
+      }
     }
   }
   __syncthreads();
   if (S.bad) return;
-  // ranks: counting sort by (length, symbol); S.fill[ln] = next free index
+  // ranks: counting sort by (length, symbol).  Per 1024-symbol block: a
+  // symbol's rank among its warp's peers (match_any), the peers in earlier
+  // warps (one warp per length scans the 32 warp counts), and S.fill[ln],
+  // the symbols of that length in earlier blocks.
   const unsigned lt = (1u << lane) - 1;
   for (uint32_t b0 = 0; b0 < alphabet; b0 += K1_THREADS) {
     const uint32_t s = b0 + tid;
@@ -385,9 +429,22 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
     __syncwarp();
     if (ln && wrank == 0) S.wcnt[warp][ln] = __popc(peers);
     __syncthreads();
+    {  // warp v scans the per-warp counts of length v + 1
+      const uint32_t lv = warp + 1;
+      const uint32_t v = S.wcnt[lane][lv];
+      uint32_t x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      S.wpre[lane][lv] = S.fill[lv] + x - v;
+      __syncwarp();
+      if (lane == 31) S.fill[lv] += x;
+    }
+    __syncthreads();
     if (ln) {
-      uint32_t r = S.fill[ln] + wrank;
-      for (int w = 0; w < warp; ++w) r += S.wcnt[w][ln];
+      const uint32_t r = S.wpre[warp][ln] + wrank;
       if (ln <= (uint32_t)FB && r < FB_SIZE) S.sym[r] = (uint16_t)s;
       // the global long-code arrays: one CTA per 1024-symbol block
       if ((b0 / K1_THREADS) % G == cta) {
@@ -396,12 +453,6 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
         ljsym[r] = (uint16_t)s;
         ljlen[r] = (uint8_t)ln;
       }
-    }
-    __syncthreads();
-    if (tid >= 1 && tid <= 32) {
-      uint32_t add = 0;
-      for (int w = 0; w < K1_THREADS / 32; ++w) add += S.wcnt[w][tid];
-      S.fill[tid] += add;
     }
     __syncthreads();
   }
@@ -425,7 +476,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
       // every whole codeword of the 12-bit window (zero fill past it cannot
       // change a match that lies inside it): start mask and end; the first six
       // also for the multi-symbol decode table
-      uint32_t pos = 0, starts = 0, n6 = 0, l0 = 0, p6 = 0, sx = 0, sy = 0, sz = 0;
+      uint32_t pos = 0, starts = 0, n6 = 0, l0 = 0, p6 = 0, p3 = 0, sx = 0, sy = 0, sz = 0;
       while (pos < (uint32_t)FB) {
         const uint32_t e = pos ? canon_one(S, w0 << pos) : e0;
         const uint32_t len = (e >> 16) & 0xffu;
@@ -435,8 +486,14 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
           if (n6 == 0) l0 = len;
           pack6(sx, sy, sz, n6++, e & 0xffffu);
           p6 = pos + len;
+          if (n6 <= 3) p3 = p6;
         }
         pos += len;
+      }
+      {
+        const uint32_t n3 = n6 < 3 ? n6 : 3;
+        reinterpret_cast<uint2*>(B + L.wlut12n)[v] =
+            pack3(sx & 0xffffu, n3 > 1 ? sx >> 16 : 0u, n3 > 2 ? sy & 0xffffu : 0u, n3, l0, p3);
       }
       clut12[v] = (uint16_t)(starts | (pos << 12));
       uint4 wl;

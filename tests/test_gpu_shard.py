@@ -45,7 +45,7 @@ def test_chunked_decode_matches_whole_stream(ph, sigma, n, variant, nchunks):
         c = _lib.Stream(ds.c.words_dev + 4 * ch.word0, ch.total_bits, ch.n, lay.subseq_bits,
                         lay.subseqs_per_seq, book.symbol_width, ds.max_codes, ds.c.gap_dev + ch.sub0,
                         ds.c.table_dev, ch.first_entry, 0)
-        tune = make_tune(max_len=book.max_len)
+        tune = make_tune(max_len=book.max_len, min_len=book.min_len)
         wsb = lib.bh_workspace_bytes(C.byref(c), var, C.byref(tune))
         ws = torch.zeros(wsb, dtype=torch.uint8, device=ds.device)
         out = empty(max(ch.n, 1), np.uint16, ds.device)

@@ -37,7 +37,7 @@ def test_two_streams_in_flight(ph, variant):
         book = ph.book_for(codes, 16)
         stream = ph.encode(codes, book, ph.DEFAULT_LAYOUT, with_gap=True)
         ds = device_stream(stream)
-        tune = make_tune(max_len=book.max_len)
+        tune = make_tune(max_len=book.max_len, min_len=book.min_len)
         wsb = lib.bh_workspace_bytes(C.byref(ds.c), var, C.byref(tune))
         cs = torch.cuda.Stream()
         ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=ds.device)
@@ -86,7 +86,7 @@ def test_host_threads_decode_concurrently(ph):
         try:
             codes, st, ds = fields[k]
             var = _lib.VARIANT_GAP if k % 2 == 0 else _lib.VARIANT_SYNC
-            tune = make_tune(max_len=st.codebook.max_len)
+            tune = make_tune(max_len=st.codebook.max_len, min_len=st.codebook.min_len)
             cs = torch.cuda.Stream()
             wsb = lib.bh_workspace_bytes(C.byref(ds.c), var, C.byref(tune))
             ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=ds.device)

@@ -16,7 +16,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
-from bench import Decoder, build_field  # noqa: E402
+from bench import Piece, load_synth  # noqa: E402
 
 SLOTS = 64
 
@@ -27,13 +27,27 @@ def main():
     ap.add_argument("--variant", default="gap")
     ap.add_argument("--noflush", action="store_true")
     args = ap.parse_args()
-    spec, codes, book, stream = build_field(args.config, 0)
-    dec = Decoder(stream, args.variant)
+    import paper_2201_09118_b200 as ph
+    synth = load_synth()
+    spec = synth.FIELDS[args.config]
+    codes = synth.field_codes(spec)
+    stream = ph.encode(codes, ph.book_for(codes, 16), ph.DEFAULT_LAYOUT, with_gap=True)
+    piece = Piece(stream, args.variant)
+    piece.table_build(torch.cuda.current_stream().cuda_stream)
+
+    class Dec:  # one fused decode per call (tables already built)
+        lib = piece.lib
+        out = piece.out
+
+        def __call__(self):
+            piece.decode(torch.cuda.current_stream().cuda_stream)
+    dec = Dec()
     lib = dec.lib
     lib.bh_debug_fused_trace.argtypes = [C.c_void_p]
-    lib.bh_debug_fused_shape.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+    lib.bh_debug_fused_shape.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_uint32), C.POINTER(C.c_uint32),
+                                         C.c_void_p, C.c_void_p]
     W, sm = C.c_uint32(), C.c_uint32()
-    lib.bh_debug_fused_shape(dec.ds.ref, C.byref(dec.tune), C.byref(W), C.byref(sm))
+    lib.bh_debug_fused_shape(C.byref(piece.c), C.byref(piece.tune), C.byref(W), C.byref(sm), None, None)
     W = W.value
     nmax = 148 * 8 * W
     tr = torch.zeros(nmax * SLOTS, dtype=torch.int64, device="cuda")
