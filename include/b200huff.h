@@ -139,6 +139,22 @@ int bh_symbol_histogram(const uint16_t *symbols_dev, uint64_t n, uint32_t alphab
 int bh_build_lengths(const uint64_t *counts_dev, uint32_t alphabet, uint8_t *lengths_dev,
                      int32_t *status_dev, void *cuda_stream);
 
+/* ---- dequantization after decode (kernels.py:216-227 dequantize_chain) --
+ * out_dev[i] = the reference reconstruction of code i, float64.
+ * exact_scan = 1: one-pass segmented prefix sum (decoupled look-back) valid in
+ *   the exact regime -- twice_eb a power of two 2^e (-149 <= e <= 104), every
+ *   outlier value an integer multiple of twice_eb (outlier_units_dev = value /
+ *   twice_eb) -- as long as every running sum stays below 2^24 in magnitude;
+ *   *inexact_dev (device int32) is set otherwise (output then unspecified).
+ *   BH_BAD_ARGUMENT when twice_eb is not such a power of two.
+ * exact_scan = 0: the reference recurrence on one device thread (any regime).
+ * Outlier indices ascending; workspace from bh_dequant_workspace_bytes(n). */
+size_t bh_dequant_workspace_bytes(uint64_t n);
+int bh_dequantize(const uint16_t *codes_dev, uint64_t n, const int64_t *outlier_idx_dev,
+                  const double *outlier_val_dev, const int64_t *outlier_units_dev, uint64_t n_outliers,
+                  double twice_eb, uint32_t midpoint, int exact_scan, double *out_dev, void *workspace_dev,
+                  size_t workspace_bytes, int32_t *inexact_dev, void *cuda_stream);
+
 /* ---- whole-decoder entry point (sync_decoder.decode / gap_decoder.decode) */
 size_t bh_workspace_bytes(const bh_stream *s, int variant, const bh_tune *tune);
 /* Decodes symbol_count symbols into out_dev (uint16).  report_dev receives a

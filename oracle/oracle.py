@@ -73,6 +73,7 @@ def lib():
         _lib.or_canonical_table.argtypes = [P, I, P, P, P, P, P]
         _lib.or_canonical_table.restype = C.c_int32
         _lib.or_tuner_plan.argtypes = [P, I, I, I, I, I, P, P, P, P]
+        _lib.or_dequantize.argtypes = [P, I, P, P, I, C.c_double, I, P]
     return _lib
 
 
@@ -348,3 +349,14 @@ def sync_decode(stream, capacity: int = 3584):
 
 if __name__ == "__main__":  # pragma: no cover
     print(build())
+
+
+def dequantize(codes, outlier_indices, outlier_values, twice_eb: float, midpoint: int) -> np.ndarray:
+    """kernels.py:216-227 dequantize_chain (float32-rounded recurrence)."""
+    c = np.ascontiguousarray(codes, dtype=np.uint16)
+    oi = np.ascontiguousarray(outlier_indices, dtype=np.int64)
+    ov = np.ascontiguousarray(outlier_values, dtype=np.float64)
+    out = np.empty(c.size, dtype=np.float64)
+    lib().or_dequantize(c.ctypes.data, c.size, oi.ctypes.data, ov.ctypes.data, oi.size, float(twice_eb),
+                        int(midpoint), out.ctypes.data)
+    return out

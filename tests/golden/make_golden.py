@@ -7,6 +7,7 @@ Run in the build container only (it imports parhuff from
 
 Outputs (committed):
   tests/golden/cases/<name>.npz  -- stream + every reference output the tests pin
+  tests/golden/quant.npz         -- reference quantize/dequantize fixtures (`--quant`)
   tests/golden/digests.json      -- sha256 digests for full-size synthetic fields
                                     (`--digests [keys]`: only these, every
                                     BASELINE config by default)
@@ -297,8 +298,39 @@ def make_digests(keys=DIGEST_KEYS):
         del codes, stream, dec
         path.write_text(json.dumps(digests, indent=1) + "\n")
 
+def make_quant():
+    """Reconstruction fixtures (quant.py:50-74, kernels.py:181-227): the real
+    reference quantizes synthetic fields and dequantizes them; the decoded
+    codes, outlier sidecar and float64 reconstruction are kept."""
+    rng = np.random.default_rng(77)
+    cases = {}
+
+    def rec(name, data, eb, width=16):
+        cfg = ph.QuantConfig(error_bound=eb, symbol_width=width)
+        q = ph.quantize(data, cfg)
+        out = ph.dequantize(q, cfg)
+        cases[name] = dict(codes=q.codes, oidx=q.outlier_indices, oval=q.outlier_values, eb=np.float64(eb),
+                           width=np.int64(width), expect=out)
+        print(name, "n", len(data), "outliers", len(q.outlier_indices))
+
+    walk = np.cumsum(rng.normal(0, 0.01, 60_000))
+    rec("walk_pow2", walk, 2.0 ** -9)                      # exact regime, no outliers
+    jumps = walk.copy()
+    jumps[rng.choice(len(jumps), 40, replace=False)] += rng.normal(0, 500, 40)
+    rec("jumps_pow2", jumps, 2.0 ** -9)                    # outliers with arbitrary values
+    rec("walk_1e-3", walk, 1e-3)                           # 2eb not a power of two
+    rec("walk_w8", np.cumsum(rng.normal(0, 0.002, 30_000)), 2.0 ** -10, width=8)
+    ramp = np.arange(200_000, dtype=np.float64) * (2.0 ** -6) * 120.0  # running sums pass 2^24 units
+    rec("ramp_pow2", ramp, 2.0 ** -7)
+    sine = np.sin(np.arange(80_000) / 300.0) * 3.0
+    rec("sine_pow2_small_eb", sine, 2.0 ** -20)
+    np.savez_compressed(HERE / "quant.npz", **{f"{k}__{f}": v for k, d in cases.items() for f, v in d.items()})
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1 and sys.argv[1] == "--digests":
         make_digests(tuple(sys.argv[2:]) or DIGEST_KEYS)
+    elif len(sys.argv) > 1 and sys.argv[1] == "--quant":
+        make_quant()
     else:
         main()
