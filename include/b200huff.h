@@ -57,8 +57,14 @@ typedef struct bh_stream {
     uint32_t first_entry;        /* bit offset of the first codeword start; 0 for a whole
                                     stream, the chunk's first gap byte for a sequence-aligned
                                     chunk of a longer stream (sharded decode; fused path only) */
-    uint32_t reserved;
+    uint32_t flags;              /* BH_STREAM_* (0 for a whole stream) */
 } bh_stream;
+
+/* flags: symbol_count is only the output capacity of a chunk whose count is
+ * not known (a shard read straight from a container): the decode reports the
+ * count in bh_report.total_symbols and fails with BH_TRUNCATED only if it
+ * exceeds the capacity (fused path only). */
+#define BH_STREAM_COUNT_IS_CAPACITY 1u
 
 /* Tuning knobs (tuner.py:29-40 TunerConfig, staging.py:28 DEFAULT_CAPACITY). */
 typedef struct bh_tune {

@@ -19,6 +19,7 @@ BH_OK, BH_INVALID, BH_TRUNCATED, BH_BADGAP, BH_NOFIXPOINT = 0, 1, 2, 3, 4
 BH_NOTPRESENT, BH_GAPOVERFLOW, BH_BAD_ARGUMENT, BH_CUDA_ERROR, BH_NEED_STAGED = 5, 6, 7, 8, 9
 BH_LENGTHOVERFLOW, BH_EMPTY = 10, 11
 VARIANT_GAP, VARIANT_SYNC, VARIANT_COARSE = 1, 2, 3
+STREAM_COUNT_IS_CAPACITY = 1
 WORD_PAD = 8
 
 P = C.c_void_p
@@ -33,7 +34,7 @@ class Stream(C.Structure):
         ("words_dev", P), ("total_bits", U64), ("symbol_count", U64),
         ("subseq_bits", U32), ("subseqs_per_seq", U32), ("symbol_width", U32),
         ("max_codes", U32), ("gap_dev", P), ("table_dev", P),
-        ("first_entry", U32), ("reserved", U32),
+        ("first_entry", U32), ("flags", U32),
     ]
 
 

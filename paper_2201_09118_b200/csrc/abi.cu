@@ -297,7 +297,7 @@ extern "C" int bh_decode_async(const bh_stream* s, int variant, const bh_tune* t
     return bh_fused_decode(s, variant, tune, out_dev, ws, ws_bytes, report_dev, cuda_stream);
   // chunked streams (first_entry) are fused-path only, and need a 16-byte
   // aligned payload (shard.chunk_stream cuts at 128-bit multiples)
-  if (s->first_entry) return BH_BAD_ARGUMENT;
+  if (s->first_entry || (s->flags & BH_STREAM_COUNT_IS_CAPACITY)) return BH_BAD_ARGUMENT;
   int rc = bh_report_init(report_dev, cuda_stream);
   if (rc) return rc;
   if (s->total_bits == 0) {
@@ -333,7 +333,7 @@ extern "C" int bh_decode(const bh_stream* s, int variant, const bh_tune* tune, u
     // the fused path declined (incomplete codebook): the reference-structured
     // pipeline reproduces the reference's speculative windows exactly.  It
     // decodes whole streams only: a chunk (first_entry != 0) cannot take it.
-    if (s->first_entry) return BH_BAD_ARGUMENT;
+    if (s->first_entry || (s->flags & BH_STREAM_COUNT_IS_CAPACITY)) return BH_BAD_ARGUMENT;
     if ((rc = bh_report_init(rep, cuda_stream))) return rc;
     if ((rc = staged_pipeline(s, variant, tune, out_dev, ws, need, rep, cuda_stream, true))) return rc;
     if ((rc = bh_report_read(rep, &r, cuda_stream))) return rc;

@@ -315,7 +315,7 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
 // symbol by base[len] + code -- no per-entry global binary search.
 // ---------------------------------------------------------------------------
 constexpr int K1_THREADS = 1024;  // 32 warps: one per code length in the rank scan
-constexpr int K1_GRID = 8;
+constexpr int K1_GRID = 16;
 
 struct CanonSmem {
   unsigned long long lim[33];
@@ -325,6 +325,7 @@ struct CanonSmem {
   uint32_t wcnt[K1_THREADS / 32][33];
   uint32_t wpre[K1_THREADS / 32][33];
   uint16_t sym[FB_SIZE];  // canonical order of the codes of length <= 12
+  uint32_t l12[FB_SIZE];  // sym | len<<16 of the codeword at each 12-bit prefix (codes <= 12 bits)
   int bad;
 };
 
@@ -456,8 +457,18 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
     }
     __syncthreads();
   }
-  // direct tables: 12-bit (lut12, clut12, wlut12), 11-bit (lut, cnt) and
-  // 8-bit (dlut8, clut8, wlut8) entries spread over every thread of the grid
+  // every codeword of <= 12 bits by its 12-bit prefix (one limit search per
+  // entry, in every CTA); the direct tables then walk windows through it
+  for (uint32_t v = tid; v < FB_SIZE; v += K1_THREADS) {
+    const uint32_t e = canon_one(S, v << (32 - FB));
+    S.l12[v] = ((e >> 16) & 0xffu) <= (uint32_t)FB ? e : 0u;
+  }
+  __syncthreads();
+  // direct tables: 12-bit (lut12, clut12, wlut12, wlut12n), 11-bit (lut, cnt)
+  // and 8-bit (dlut8, clut8, wlut8) entries spread over every thread of the
+  // grid.  A codeword at offset pos of a W-bit window v is S.l12 of the 12
+  // bits (v << (12 - W + pos)), zero-filled: it lies inside the window when
+  // pos + len <= W (zero fill past the window cannot change such a match).
   TableLayout L(max_codes);
   char* B = static_cast<char*>(blob);
   uint32_t* lut12 = reinterpret_cast<uint32_t*>(B + L.lut12);
@@ -468,77 +479,46 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   uint4* wlut8 = reinterpret_cast<uint4*>(B + L.wlut8);
   constexpr uint32_t N12 = FB_SIZE, N11 = LUT_SIZE, N8 = 256;
   for (uint32_t it = cta * K1_THREADS + tid; it < N12 + N11 + N8; it += G * K1_THREADS) {
+    const uint32_t W = it < N12 ? (uint32_t)FB : it < N12 + N11 ? (uint32_t)LUT_BITS : 8u;
+    const uint32_t v = it < N12 ? it : it < N12 + N11 ? it - N12 : it - N12 - N11;
+    const uint32_t v12 = v << (FB - W);
+    const uint32_t e0 = S.l12[v12];
+    // every whole codeword of the window: start mask, end, count; the first
+    // six (three) also for the multi-symbol decode tables
+    uint32_t pos = 0, starts = 0, n = 0, n6 = 0, l0 = 0, p6 = 0, p3 = 0, sx = 0, sy = 0, sz = 0;
+    while (pos < W) {
+      const uint32_t e = pos ? S.l12[(v12 << pos) & (FB_SIZE - 1)] : e0;
+      const uint32_t len = (e >> 16) & 0xffu;
+      if (len == 0 || pos + len > W) break;
+      starts |= 1u << pos;
+      if (n6 < 6) {
+        if (n6 == 0) l0 = len;
+        pack6(sx, sy, sz, n6++, e & 0xffffu);
+        p6 = pos + len;
+        if (n6 <= 3) p3 = p6;
+      }
+      pos += len;
+      ++n;
+    }
+    const uint32_t first = ((e0 >> 16) & 0xffu) <= W ? e0 : 0u;
+    uint4 wl;
+    wl.x = sx;
+    wl.y = sy;
+    wl.z = sz;
     if (it < N12) {
-      const uint32_t v = it;
-      const uint32_t w0 = v << (32 - FB);
-      const uint32_t e0 = canon_one(S, w0);
-      lut12[v] = ((e0 >> 16) & 0xffu) <= (uint32_t)FB ? e0 : 0u;
-      // every whole codeword of the 12-bit window (zero fill past it cannot
-      // change a match that lies inside it): start mask and end; the first six
-      // also for the multi-symbol decode table
-      uint32_t pos = 0, starts = 0, n6 = 0, l0 = 0, p6 = 0, p3 = 0, sx = 0, sy = 0, sz = 0;
-      while (pos < (uint32_t)FB) {
-        const uint32_t e = pos ? canon_one(S, w0 << pos) : e0;
-        const uint32_t len = (e >> 16) & 0xffu;
-        if (len == 0 || pos + len > (uint32_t)FB) break;
-        starts |= 1u << pos;
-        if (n6 < 6) {
-          if (n6 == 0) l0 = len;
-          pack6(sx, sy, sz, n6++, e & 0xffffu);
-          p6 = pos + len;
-          if (n6 <= 3) p3 = p6;
-        }
-        pos += len;
-      }
-      {
-        const uint32_t n3 = n6 < 3 ? n6 : 3;
-        reinterpret_cast<uint2*>(B + L.wlut12n)[v] =
-            pack3(sx & 0xffffu, n3 > 1 ? sx >> 16 : 0u, n3 > 2 ? sy & 0xffffu : 0u, n3, l0, p3);
-      }
+      lut12[v] = first;
       clut12[v] = (uint16_t)(starts | (pos << 12));
-      uint4 wl;
-      wl.x = sx;
-      wl.y = sy;
-      wl.z = sz;
       wl.w = n6 ? (p6 | (n6 << 4) | (l0 << 16) | ((2 * n6) << 28)) : 0u;
       wlut12[v] = wl;
+      const uint32_t n3 = n6 < 3 ? n6 : 3;
+      reinterpret_cast<uint2*>(B + L.wlut12n)[v] =
+          pack3(sx & 0xffffu, n3 > 1 ? sx >> 16 : 0u, n3 > 2 ? sy & 0xffffu : 0u, n3, l0, p3);
     } else if (it < N12 + N11) {
-      const uint32_t v = it - N12;
-      const uint32_t w0 = v << (32 - LUT_BITS);
-      const uint32_t e0 = canon_one(S, w0);
-      lut[v] = ((e0 >> 16) & 0xffu) <= (uint32_t)LUT_BITS ? e0 : 0u;
-      uint32_t pos = 0, n = 0;
-      while (pos < (uint32_t)LUT_BITS) {
-        const uint32_t e = pos ? canon_one(S, w0 << pos) : e0;
-        const uint32_t len = (e >> 16) & 0xffu;
-        if (len == 0 || pos + len > (uint32_t)LUT_BITS) break;
-        pos += len;
-        ++n;
-      }
+      lut[v] = first;
       cnt[v] = n ? (uint16_t)(pos | (n << 8)) : (uint16_t)0;
     } else {
-      const uint32_t v = it - N12 - N11;
-      const uint32_t w0 = v << 24;
-      const uint32_t e0 = canon_one(S, w0);
-      dlut8[v] = ((e0 >> 16) & 0xffu) <= 8u ? e0 : 0u;
-      uint32_t pos = 0, n = 0, n6 = 0, p6 = 0, l0 = 0, sx = 0, sy = 0, sz = 0;
-      while (pos < 8) {
-        const uint32_t e = pos ? canon_one(S, w0 << pos) : e0;
-        const uint32_t len = (e >> 16) & 0xffu;
-        if (len == 0 || pos + len > 8) break;
-        if (n6 < 6) {
-          if (n6 == 0) l0 = len;
-          pack6(sx, sy, sz, n6++, e & 0xffffu);
-          p6 = pos + len;
-        }
-        pos += len;
-        ++n;
-      }
+      dlut8[v] = first;
       clut8[v] = n ? (uint8_t)((n << 3) | (pos - 1)) : (uint8_t)0;
-      uint4 wl;
-      wl.x = sx;
-      wl.y = sy;
-      wl.z = sz;
       wl.w = n6 ? (p6 | (n6 << 4) | (n << 8) | (pos << 12) | (l0 << 16) | ((2 * n6) << 28)) : 0u;
       wlut8[v] = wl;
     }

@@ -126,6 +126,27 @@ class DeviceStream:
                              lay.subseqs_per_seq, book.symbol_width, self.max_codes,
                              ptr(self.gap), ptr(self.table))
 
+    @classmethod
+    def from_device(cls, stream, words, gap, device) -> "DeviceStream":
+        """Mirror over device buffers that already hold the payload words (+ pad)
+        and gap bytes (container ingest); builds the K1 tables."""
+        lib = load()
+        ds = cls.__new__(cls)
+        ds.device = device
+        ds.stream = stream
+        ds.words = words
+        ds.gap = gap
+        book = stream.codebook
+        lay = stream.layout
+        ds.max_codes = max(len(book.entries), 1)
+        ds.table = empty(lib.bh_table_bytes(ds.max_codes), np.uint8, device)
+        lens = book.length_bytes()
+        ds._lens = h2d(lens if lens.size else np.zeros(1, np.uint8), device)
+        check(lib.bh_table_build(ptr(ds._lens), len(lens), ptr(ds.table), ds.max_codes, stream_handle()), "table")
+        ds.c = _lib.Stream(ptr(words), int(stream.total_bits), int(stream.symbol_count), lay.subseq_bits,
+                           lay.subseqs_per_seq, book.symbol_width, ds.max_codes, ptr(gap), ptr(ds.table))
+        return ds
+
     @property
     def ref(self):
         return C.byref(self.c)

@@ -2,9 +2,11 @@
 
 Decoding shards with no collective on the data path:
 
-* a batch of independent fields (the multi-field config) is spread over ranks
-  by longest-processing-time on payload bits, every rank decoding its own
-  fields into its own output;
+* a batch of independent fields (the multi-field config) is cut into `world`
+  equal contiguous spans of sequences (``balanced_pieces``: payload bits per
+  sequence are constant, and decode time follows payload bits), each rank
+  decoding its pieces concurrently into its own outputs (``decode_shard``);
+  ``lpt_assign`` spreads whole fields instead;
 * one long stream is cut at sequence boundaries, so every shard's entry bits
   are known (boundary + gap byte) and shards are independent; the only
   exchange is the per-shard symbol totals (8 bytes per rank) that place each
@@ -169,3 +171,77 @@ def piece_chunk(total_bits: int, subseq_bits: int, subseqs_per_seq: int, gap, su
     gap = np.asarray(gap, dtype=np.int64)
     oi = np.concatenate([[0], np.cumsum(np.asarray(subseq_counts, dtype=np.int64))])
     return _chunk(q0, q1, total_bits, subseq_bits, subseqs_per_seq, gap, oi)
+
+
+def decode_shard(streams, rank: int = 0, world: int = 1, variant: str = "gap", device=None):
+    """Decode this rank's share of a batch of streams (BASELINE
+    config 5): the batch's sequences cut into `world` equal contiguous spans
+    (`balanced_pieces`), each piece a sequence-aligned chunk entered at its
+    first gap byte.  The pieces run as concurrent fused decodes on one CUDA
+    stream each, their CTA counts proportional to their payload, so the rank's
+    whole share takes one wave of the GPU.  No collective: the result is, per
+    piece, (stream index, output offset in that stream, device uint16 tensor).
+    Streams need their gap arrays (every piece's entry bit and symbol count
+    come from them and the encode-side count pass)."""
+    import ctypes as C
+
+    import torch
+
+    from . import _lib
+    from ._lib import check, stream_handle
+    from ._pipeline import make_tune
+    from .device import DeviceReport, device_stream, empty
+    from .gap_decoder import count_pass, entries_from_gap
+    from .errors import NotPresent
+    lib = _lib.load()
+    var = _lib.VARIANT_GAP if variant == "gap" else _lib.VARIANT_SYNC
+    for st in streams:
+        if st.gap is None:
+            raise NotPresent("sharded decode needs every stream's gap array")
+    spans = balanced_pieces([st.num_seqs for st in streams], world)[rank]
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    main = torch.cuda.current_stream(dev)
+    total_bits = 0
+    plan = []
+    for fi, q0, q1 in spans:
+        st = streams[fi]
+        ds = device_stream(st, dev)
+        lay = st.layout
+        if q0 == 0 and q1 == st.num_seqs:
+            c = _lib.Stream(ds.c.words_dev, st.total_bits, st.symbol_count, lay.subseq_bits, lay.subseqs_per_seq,
+                            st.codebook.symbol_width, ds.max_codes, ds.c.gap_dev, ds.c.table_dev, 0, 0)
+            n, out0, tb = st.symbol_count, 0, st.total_bits
+        else:
+            s = entries_from_gap(st)
+            count_pass(st, s)
+            ch = piece_chunk(st.total_bits, lay.subseq_bits, lay.subseqs_per_seq, st.gap, s.counts, q0, q1)
+            c = _lib.Stream(ds.c.words_dev + 4 * ch.word0, ch.total_bits, ch.n, lay.subseq_bits, lay.subseqs_per_seq,
+                            st.codebook.symbol_width, ds.max_codes, ds.c.gap_dev + ch.sub0, ds.c.table_dev,
+                            ch.first_entry, 0)
+            n, out0, tb = ch.n, ch.out0, ch.total_bits
+        plan.append((fi, out0, n, tb, c, st.codebook))
+        total_bits += tb
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    results, keep = [], []
+    for k, (fi, out0, n, tb, c, book) in enumerate(plan):
+        tune = make_tune(max_len=book.max_len, min_len=book.min_len)
+        if len(plan) > 1:
+            tune.ctas = max(1, round(sms * tb / max(total_bits, 1)))
+        s = torch.cuda.Stream(dev) if k else main
+        if k:
+            s.wait_stream(main)
+        with torch.cuda.stream(s):
+            out = empty(n, np.uint16, dev)
+            wsb = lib.bh_workspace_bytes(C.byref(c), var, C.byref(tune))
+            ws = torch.empty(max(wsb, 256), dtype=torch.uint8, device=dev)  # this call's scratch
+            check(lib.bh_workspace_reset(ws.data_ptr(), ws.numel(), stream_handle(s)), "workspace")
+            rep = DeviceReport(dev).init()
+            check(lib.bh_decode_async(C.byref(c), var, C.byref(tune), out.data_ptr(), ws.data_ptr(), wsb, rep.ptr,
+                                      stream_handle(s)), "shard decode")
+        keep.append((s, rep, c, tune, ws))
+        results.append((fi, out0, out[:n]))
+    for s, rep, *_ in keep:
+        main.wait_stream(s)
+        with torch.cuda.stream(s):
+            check(rep.read().status, "shard decode")
+    return results

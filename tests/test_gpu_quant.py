@@ -77,7 +77,8 @@ def test_decode_then_dequantize_on_device(ph, oracle_mod, variant):
     """Decode a field and reconstruct it without the codes leaving the GPU."""
     from paper_2201_09118_b200 import quant
     from paper_2201_09118_b200.synth import gaussian_codes
-    codes = gaussian_codes(5_000_000, 1024, 3.0, seed=11)
+    # quantization codes around the 16-bit midpoint (cuSZ-style)
+    codes = (gaussian_codes(5_000_000, 1024, 3.0, seed=11).astype(np.int64) - 512 + 32768).astype(np.uint16)
     st = ph.encode(codes, ph.book_for(codes, 16), ph.DEFAULT_LAYOUT, with_gap=True)
     cfg = quant.QuantConfig(2.0 ** -9, 16)
     oidx = np.array([0, 17, 4096, 4_999_999], np.int64)

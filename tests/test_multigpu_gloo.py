@@ -63,3 +63,53 @@ def test_sequence_ranges_cover_stream():
             assert rs[0][0] == 0 and rs[-1][1] == nseq
             assert all(a[1] == b[0] for a, b in zip(rs, rs[1:]))
             assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
+
+
+def _pieces_worker(rank, world, port, nseqs, q):
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        mine = shard.balanced_pieces(nseqs, world)[rank]
+        totals = shard.gather_totals(sum(q1 - q0 for _, q0, q1 in mine))
+        q.put((rank, mine, totals))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_rank_balanced_pieces_gloo():
+    """Strong-scaling split of a batch (BASELINE config 5) over 2 ranks: every
+    sequence of every field on exactly one rank, equal shares (+-1)."""
+    nseqs = [67_123, 22_240, 251_255]
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_pieces_worker, args=(r, world, port, nseqs, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    totals = res[0][2]
+    assert res[1][2] == totals and sum(totals) == sum(nseqs) and abs(totals[0] - totals[1]) <= 1
+    seen = {f: [] for f in range(len(nseqs))}
+    for _, mine, _ in res:
+        for f, q0, q1 in mine:
+            seen[f].append((q0, q1))
+    for f, n in enumerate(nseqs):
+        spans = sorted(seen[f])
+        assert spans[0][0] == 0 and spans[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(spans, spans[1:]))
+
+
+def test_balanced_pieces_many_worlds():
+    nseqs = [5, 0, 17, 3]
+    for world in (1, 2, 3, 4, 8, 30):
+        parts = shard.balanced_pieces(nseqs, world)
+        assert len(parts) == world
+        assert sum(q1 - q0 for p in parts for _, q0, q1 in p) == sum(nseqs)
+        sizes = [sum(q1 - q0 for _, q0, q1 in p) for p in parts]
+        assert max(sizes) - min(sizes) <= 1
