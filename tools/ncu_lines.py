@@ -7,7 +7,9 @@ from collections import defaultdict
 
 rep = sys.argv[1]
 top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
+import os
+extra = ["--kernel-name", os.environ["NCU_KERNEL"], "--launch-count", "1"] if os.environ.get("NCU_KERNEL") else []
+txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"] + extra,
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
 agg = defaultdict(lambda: [0, 0, ""])
@@ -35,5 +37,6 @@ for r in rows:
 tot = sum(v[0] for v in agg.values()) or 1
 ts = sum(v[1] for v in agg.values()) or 1
 print(f"total instructions {tot}  stall samples {ts}")
-for k, v in sorted(agg.items(), key=lambda kv: -kv[1][0])[:top]:
+key = 1 if os.environ.get("NCU_SORT") == "stall" else 0
+for k, v in sorted(agg.items(), key=lambda kv: -kv[1][key])[:top]:
     print(f"{k[0]}:{k[1]:<5} {100 * v[0] / tot:5.1f}% instr {100 * v[1] / ts:5.1f}% stall  {v[2].strip()}")
