@@ -9,8 +9,10 @@
 // S_i of (code - midpoint) since the last outlier (plus the outlier's value in
 // units of 2^e) stays below 2^24 in magnitude, every step is exact -- the f64
 // product and sum are exact and the f32 rounding keeps all 24 significant
-// bits -- so pred_i = 2^e * S_i: a segmented prefix sum, computed here in one
-// pass with a decoupled look-back across tiles.  The kernel raises a device
+// bits -- so pred_i = 2^e * S_i: a segmented prefix sum, computed here as
+// reduce (tile aggregates) -> scan (one CTA) -> apply.  (A one-pass decoupled
+// look-back spent half its time with whole CTAs parked at the look-back
+// barrier: 1.48 ms for 281 M codes, 28 % of HBM; profiles/r02.)  The kernel raises a device
 // flag when a running sum leaves that range; the caller then runs the exact
 // sequential chain on the device (k_dequant_chain, one thread: slow but
 // bit-identical in every regime).
@@ -23,21 +25,11 @@ constexpr int DQ_ITEMS = 16;                        // codes per thread
 constexpr int DQ_TILE = DQ_THREADS * DQ_ITEMS;      // 4096 codes per tile
 constexpr long long DQ_LIMIT = 1ll << 24;
 
-// descriptor: [63:62] 0 empty / 1 aggregate / 2 inclusive, [61] segment reset
-// inside, [60:0] sum (two's complement)
-constexpr unsigned long long DQ_AGG = 1ull << 62, DQ_INC = 2ull << 62, DQ_RST = 1ull << 61;
-constexpr unsigned long long DQ_VAL = (1ull << 61) - 1;
 
 struct DqWork {
-  unsigned long long tiles;  // dynamic tile counter
-  int32_t inexact;           // a running sum left +-2^24 (or a flagged outlier)
-  int32_t pad;
-  unsigned long long desc[1];
+  int32_t inexact;  // a running sum left +-2^24 (or a tile held more than 64 outliers)
+  int32_t pad[3];
 };
-
-__device__ __forceinline__ long long dq_sext(unsigned long long v) {
-  return (long long)(v << 3) >> 3;  // 61-bit two's complement
-}
 
 struct Seg {  // segmented-sum scan element
   long long s;
@@ -45,26 +37,27 @@ struct Seg {  // segmented-sum scan element
 };
 __device__ __forceinline__ Seg seg_op(Seg a, Seg b) { return b.r ? b : Seg{a.s + b.s, a.r}; }
 
-__global__ void __launch_bounds__(DQ_THREADS) k_dequant(const uint16_t* __restrict__ codes, uint64_t n,
-                                                        const int64_t* __restrict__ oidx,
-                                                        const long long* __restrict__ ounits, uint64_t nout,
-                                                        double twice_eb, int32_t mid, double* __restrict__ out,
-                                                        DqWork* w) {
-  __shared__ uint32_t s_tile;
-  __shared__ Seg s_warp[DQ_THREADS / 32];
-  __shared__ long long s_prefix;
+// Per tile (DQ_TILE codes): this thread's 16 deltas (code - midpoint, or an
+// outlier's value in units of twice_eb with its reset bit), and the block's
+// segmented scan of the thread totals.  Shared by the reduce and apply passes.
+struct DqTile {
+  long long v[DQ_ITEMS];
+  uint32_t rmask;
+  Seg x;    // inclusive scan of thread totals within its warp
+  Seg agg;  // tile aggregate
+};
+
+__device__ __forceinline__ void dq_tile(const uint16_t* __restrict__ codes, uint64_t n,
+                                        const int64_t* __restrict__ oidx, const long long* __restrict__ ounits,
+                                        uint64_t nout, int32_t mid, uint64_t tile, DqWork* w, DqTile& T,
+                                        Seg* s_warp) {
   __shared__ uint32_t s_rst[DQ_TILE / 32];  // outlier positions of the tile (bitmask)
   __shared__ long long s_oval[64];          // their values in units of twice_eb (first 64 per tile)
   __shared__ uint32_t s_nout, s_o0;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_tile = (uint32_t)atomicAdd(&w->tiles, 1ull);
-  for (uint32_t i = tid; i < DQ_TILE / 32; i += DQ_THREADS) s_rst[i] = 0;
-  __syncthreads();
-  const uint64_t tile = s_tile;
   const uint64_t t0 = tile * DQ_TILE;
-  if (t0 >= n) return;
-  // outliers of this tile: binary search for the first index >= t0
-  if (tid == 0) {
+  for (uint32_t i = tid; i < DQ_TILE / 32; i += DQ_THREADS) s_rst[i] = 0;
+  if (tid == 0) {  // outliers of this tile: first index >= t0
     uint64_t lo = 0, hi = nout;
     while (lo < hi) {
       const uint64_t m = (lo + hi) >> 1;
@@ -74,7 +67,7 @@ __global__ void __launch_bounds__(DQ_THREADS) k_dequant(const uint16_t* __restri
     while (e < nout && (uint64_t)oidx[e] < t0 + DQ_TILE) ++e;
     s_o0 = (uint32_t)lo;
     s_nout = (uint32_t)(e - lo);
-    if (e - lo > 64) w->inexact = 1;  // more than 64 outliers in 4096 codes: take the exact chain
+    if (e - lo > 64 && w) w->inexact = 1;  // more than 64 outliers in 4096 codes: take the exact chain
   }
   __syncthreads();
   const uint32_t no = min(s_nout, 64u);
@@ -84,36 +77,33 @@ __global__ void __launch_bounds__(DQ_THREADS) k_dequant(const uint16_t* __restri
     s_oval[k] = ounits[s_o0 + k];
   }
   __syncthreads();
-  // this thread's 16 codes: deltas, local segmented scan
   const uint64_t i0 = t0 + (uint64_t)tid * DQ_ITEMS;
-  long long v[DQ_ITEMS];
-  uint32_t rmask = 0;
   const uint32_t rbits = (s_rst[(tid * DQ_ITEMS) >> 5] >> ((tid * DQ_ITEMS) & 31)) & 0xffffu;
   if (i0 + DQ_ITEMS <= n) {
     const uint4* src = reinterpret_cast<const uint4*>(codes + i0);
     const uint4 a = __ldg(src), b = __ldg(src + 1);
     const uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
 #pragma unroll
-    for (int k = 0; k < DQ_ITEMS; ++k) v[k] = (long long)((wv[k >> 1] >> ((k & 1) * 16)) & 0xffffu) - mid;
+    for (int k = 0; k < DQ_ITEMS; ++k) T.v[k] = (long long)((wv[k >> 1] >> ((k & 1) * 16)) & 0xffffu) - mid;
   } else {
 #pragma unroll
-    for (int k = 0; k < DQ_ITEMS; ++k) v[k] = i0 + k < n ? (long long)codes[i0 + k] - mid : 0ll;
+    for (int k = 0; k < DQ_ITEMS; ++k) T.v[k] = i0 + k < n ? (long long)codes[i0 + k] - mid : 0ll;
   }
+  T.rmask = 0;
   if (rbits) {
     uint32_t oi = 0;  // rank of this thread's first outlier among the tile's
     for (uint32_t q = 0; q < (tid * DQ_ITEMS) >> 5; ++q) oi += __popc(s_rst[q]);
     oi += __popc(s_rst[(tid * DQ_ITEMS) >> 5] & ((1u << ((tid * DQ_ITEMS) & 31)) - 1u));
 #pragma unroll
     for (int k = 0; k < DQ_ITEMS; ++k)
-      if ((rbits >> k) & 1u) { v[k] = s_oval[oi++]; rmask |= 1u << k; }
+      if ((rbits >> k) & 1u) { T.v[k] = s_oval[oi++]; T.rmask |= 1u << k; }
   }
   Seg t{0, 0};
 #pragma unroll
   for (int k = 0; k < DQ_ITEMS; ++k) {
-    if ((rmask >> k) & 1u) t = Seg{v[k], 1};
-    else t.s += v[k];
+    if ((T.rmask >> k) & 1u) t = Seg{T.v[k], 1};
+    else t.s += T.v[k];
   }
-  // block-wide exclusive segmented scan of the thread totals
   Seg x = t;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -130,59 +120,93 @@ __global__ void __launch_bounds__(DQ_THREADS) k_dequant(const uint16_t* __restri
       if ((int)lane >= o) z = seg_op(y, z);
     }
     if (lane < DQ_THREADS / 32) s_warp[lane] = z;  // inclusive per warp
-    // tile aggregate -> look-back (lane 0 publishes, the warp looks back)
-    const Seg agg{__shfl_sync(0xffffffffu, z.s, DQ_THREADS / 32 - 1),
-                  __shfl_sync(0xffffffffu, z.r, DQ_THREADS / 32 - 1)};
-    long long excl = 0;
-    if (tile == 0) {
-      if (lane == 0)
-        st_release(&w->desc[0], DQ_INC | (agg.r ? DQ_RST : 0ull) | ((unsigned long long)agg.s & DQ_VAL));
-    } else {
-      // a tile with an outlier knows its inclusive value at once; its codes
-      // before the outlier still need the prefix of the tiles before it
-      if (lane == 0)
-        st_release(&w->desc[tile], (agg.r ? DQ_INC : DQ_AGG) | (agg.r ? DQ_RST : 0ull) |
-                                       ((unsigned long long)agg.s & DQ_VAL));
-      {
-        // walk back until an inclusive prefix or a reset (a segment start)
-        int64_t base = (int64_t)tile - 1;
-        while (base >= 0) {
-          const int64_t idx = base - (int64_t)lane;
-          unsigned long long d;
-          while (true) {
-            d = idx >= 0 ? ld_acquire(&w->desc[idx]) : DQ_INC;
-            if (__all_sync(0xffffffffu, (d >> 62) != 0)) break;
-            __nanosleep(32);
-          }
-          const bool stop = idx < 0 || (d >> 62) == 2 || (d & DQ_RST);
-          const unsigned m = __ballot_sync(0xffffffffu, stop);
-          const uint32_t sl = m ? __ffs(m) - 1 : 31;
-          const long long val = (lane <= sl && idx >= 0) ? dq_sext(d & DQ_VAL) : 0ll;
-          excl += warp_sum(val);
-          if (m) break;
-          base -= 32;
-        }
-        if (lane == 0 && !agg.r) st_release(&w->desc[tile], DQ_INC | ((unsigned long long)(excl + agg.s) & DQ_VAL));
-      }
-    }
-    if (lane == 0) s_prefix = excl;
   }
   __syncthreads();
-  // this thread's exclusive prefix: tile prefix, then warps and lanes before it
-  Seg pre{s_prefix, 0};
+  T.x = x;
+  T.agg = s_warp[DQ_THREADS / 32 - 1];
+}
+
+// pass 1: the segmented aggregate of every tile (aggs[tile] = sum, resets[tile])
+__global__ void __launch_bounds__(DQ_THREADS) k_dq_reduce(const uint16_t* __restrict__ codes, uint64_t n,
+                                                          const int64_t* __restrict__ oidx,
+                                                          const long long* __restrict__ ounits, uint64_t nout,
+                                                          int32_t mid, long long* __restrict__ aggs,
+                                                          uint8_t* __restrict__ resets, DqWork* w) {
+  __shared__ Seg s_warp[DQ_THREADS / 32];
+  DqTile T;
+  dq_tile(codes, n, oidx, ounits, nout, mid, blockIdx.x, w, T, s_warp);
+  if (threadIdx.x == 0) {
+    aggs[blockIdx.x] = T.agg.s;
+    resets[blockIdx.x] = (uint8_t)T.agg.r;
+  }
+}
+
+// pass 2 (one CTA): exclusive segmented scan of the tile aggregates -> tile prefixes
+__global__ void __launch_bounds__(1024) k_dq_scan(long long* __restrict__ aggs, const uint8_t* __restrict__ resets,
+                                                  uint64_t ntiles) {
+  __shared__ Seg s_w[32];
+  __shared__ Seg s_carry;
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_carry = Seg{0, 0};
+  __syncthreads();
+  for (uint64_t b0 = 0; b0 < ntiles; b0 += 1024) {
+    const uint64_t i = b0 + tid;
+    const Seg a = i < ntiles ? Seg{aggs[i], resets[i]} : Seg{0, 0};
+    Seg x = a;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      Seg y{__shfl_up_sync(0xffffffffu, x.s, o), __shfl_up_sync(0xffffffffu, x.r, o)};
+      if ((int)lane >= o) x = seg_op(y, x);
+    }
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      Seg z = s_w[lane];
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        Seg y{__shfl_up_sync(0xffffffffu, z.s, o), __shfl_up_sync(0xffffffffu, z.r, o)};
+        if ((int)lane >= o) z = seg_op(y, z);
+      }
+      s_w[lane] = z;
+    }
+    __syncthreads();
+    Seg pre = s_carry;
+    if (warp) pre = seg_op(pre, s_w[warp - 1]);
+    const Seg lp{__shfl_up_sync(0xffffffffu, x.s, 1), __shfl_up_sync(0xffffffffu, x.r, 1)};
+    if (lane) pre = seg_op(pre, lp);
+    if (i < ntiles) aggs[i] = pre.s;  // exclusive prefix (the running value before the tile)
+    __syncthreads();
+    if (tid == 0) s_carry = seg_op(s_carry, s_w[31]);
+    __syncthreads();
+  }
+}
+
+// pass 3: values = 2^e * (tile prefix + in-tile segmented scan), float64 out
+__global__ void __launch_bounds__(DQ_THREADS) k_dequant(const uint16_t* __restrict__ codes, uint64_t n,
+                                                        const int64_t* __restrict__ oidx,
+                                                        const long long* __restrict__ ounits, uint64_t nout,
+                                                        double twice_eb, int32_t mid,
+                                                        const long long* __restrict__ prefix,
+                                                        double* __restrict__ out, DqWork* w) {
+  __shared__ Seg s_warp[DQ_THREADS / 32];
+  DqTile T;
+  dq_tile(codes, n, oidx, ounits, nout, mid, blockIdx.x, nullptr, T, s_warp);
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Seg pre{prefix[blockIdx.x], 0};
   if (warp) pre = seg_op(pre, s_warp[warp - 1]);
-  Seg lp{__shfl_up_sync(0xffffffffu, x.s, 1), __shfl_up_sync(0xffffffffu, x.r, 1)};
+  const Seg lp{__shfl_up_sync(0xffffffffu, T.x.s, 1), __shfl_up_sync(0xffffffffu, T.x.r, 1)};
   if (lane) pre = seg_op(pre, lp);
   long long run = pre.s;
   bool bad = false;
   double r[DQ_ITEMS];
 #pragma unroll
   for (int k = 0; k < DQ_ITEMS; ++k) {
-    run = ((rmask >> k) & 1u) ? v[k] : run + v[k];
+    run = ((T.rmask >> k) & 1u) ? T.v[k] : run + T.v[k];
     bad |= run >= DQ_LIMIT || run <= -DQ_LIMIT;
     r[k] = (double)run * twice_eb;  // exact: |run| < 2^24, twice_eb a power of two
   }
   if (bad) w->inexact = 1;
+  const uint64_t i0 = (uint64_t)blockIdx.x * DQ_TILE + (uint64_t)threadIdx.x * DQ_ITEMS;
   if (i0 + DQ_ITEMS <= n) {
     double2* dst = reinterpret_cast<double2*>(out + i0);
 #pragma unroll
@@ -213,10 +237,8 @@ __global__ void k_dequant_chain(const uint16_t* __restrict__ codes, uint64_t n, 
   }
 }
 
-__global__ void k_dq_init(DqWork* w, uint64_t ntiles) {
-  uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  if (i == 0) { w->tiles = 0; w->inexact = 0; }
-  for (; i < ntiles; i += (uint64_t)gridDim.x * blockDim.x) w->desc[i] = 0;
+__global__ void k_dq_init(DqWork* w) {
+  if (threadIdx.x == 0) w->inexact = 0;
 }
 
 }  // namespace bh
@@ -226,7 +248,7 @@ using namespace bh;
 static uint64_t dq_tiles(uint64_t n) { return (n + DQ_TILE - 1) / DQ_TILE; }
 
 extern "C" size_t bh_dequant_workspace_bytes(uint64_t n) {
-  return sizeof(DqWork) + 8 * (dq_tiles(n) + 1);
+  return align16(sizeof(DqWork)) + align16(8 * (dq_tiles(n) + 1)) + align16(dq_tiles(n) + 1);
 }
 
 // twice_eb = 2^e with -149 <= e <= 104 (f32 keeps every multiple below 2^24)
@@ -252,11 +274,20 @@ extern "C" int bh_dequantize(const uint16_t* codes_dev, uint64_t n, const int64_
         (reinterpret_cast<uintptr_t>(out_dev) & 15u))
       return BH_BAD_ARGUMENT;
     DqWork* w = static_cast<DqWork*>(ws);
-    k_dq_init<<<64, 256, 0, st>>>(w, dq_tiles(n));
-    if (n)
-      k_dequant<<<(unsigned)dq_tiles(n), DQ_THREADS, 0, st>>>(codes_dev, n, outlier_idx_dev,
-                                                             reinterpret_cast<const long long*>(outlier_units_dev),
-                                                             n_outliers, twice_eb, (int32_t)midpoint, out_dev, w);
+    const uint64_t nt = dq_tiles(n);
+    long long* aggs = reinterpret_cast<long long*>(static_cast<char*>(ws) + align16(sizeof(DqWork)));
+    uint8_t* resets = reinterpret_cast<uint8_t*>(aggs) + align16(8 * (nt + 1));
+    const long long* un = reinterpret_cast<const long long*>(outlier_units_dev);
+    k_dq_init<<<1, 32, 0, st>>>(w);
+    if (n) {
+      // reduce -> scan of the tile aggregates -> apply: every pass streams at
+      // HBM speed with no inter-CTA waiting (12 B per code in all)
+      k_dq_reduce<<<(unsigned)nt, DQ_THREADS, 0, st>>>(codes_dev, n, outlier_idx_dev, un, n_outliers,
+                                                       (int32_t)midpoint, aggs, resets, w);
+      k_dq_scan<<<1, 1024, 0, st>>>(aggs, resets, nt);
+      k_dequant<<<(unsigned)nt, DQ_THREADS, 0, st>>>(codes_dev, n, outlier_idx_dev, un, n_outliers, twice_eb,
+                                                     (int32_t)midpoint, aggs, out_dev, w);
+    }
     if (cudaMemcpyAsync(inexact_dev, &w->inexact, 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       return BH_CUDA_ERROR;
   } else {

@@ -20,7 +20,8 @@ def metrics(rep):
     hdr, units, vals = rows[0], rows[1], rows[2]
     get = lambda n: float(vals[hdr.index(n)].replace(",", "")) * UNIT.get(units[hdr.index(n)], 1)
     return {"dram_read_bytes": get("dram__bytes_read.sum"), "dram_write_bytes": get("dram__bytes_write.sum"),
-            "duration_us": float(vals[hdr.index("gpu__time_duration.sum")].replace(",", "")),
+            "duration_us": float(vals[hdr.index("gpu__time_duration.sum")].replace(",", "")) *
+            {"ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(units[hdr.index("gpu__time_duration.sum")], 1.0),
             "kernel": vals[hdr.index("Kernel Name")]}
 
 
