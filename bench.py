@@ -597,9 +597,11 @@ def build_workload(args, rank: int, world: int):
     items = [(field index, chunk or None)] is this rank's share."""
     import paper_2201_09118_b200 as ph
     from paper_2201_09118_b200 import shard
+    import torch
     fields = []
     for name, codes in workload_fields(args):
-        book = ph.book_for(codes, 16)
+        # the encode side on the device: histogram -> build_lengths -> canonize -> pack + gap
+        book = ph.book_for_device(torch.from_numpy(codes.view(np.int16)).cuda(), codes.size, 16)
         st = ph.encode(codes, book, ph.DEFAULT_LAYOUT, with_gap=True)
         fields.append((name, codes, book, st))
     if args.config != "multifield":
@@ -608,7 +610,7 @@ def build_workload(args, rank: int, world: int):
             from dataclasses import replace
             spec = replace(synth.FIELDS[args.config], seed=synth.FIELDS[args.config].seed + rank)
             codes = synth.field_codes(spec)
-            book = ph.book_for(codes, 16)
+            book = ph.book_for_device(torch.from_numpy(codes.view(np.int16)).cuda(), codes.size, 16)
             fields = [(spec.name, codes, book, ph.encode(codes, book, ph.DEFAULT_LAYOUT, with_gap=True))]
         return fields, [(0, None)]
     spans = shard.balanced_pieces([f[3].num_seqs for f in fields], world)[rank]

@@ -20,7 +20,8 @@ import numpy as np  # noqa: E402
 
 LAYOUTS = ((32, 4, 32), (32, 4, 32), (32, 4, 32), (16, 3, 5), (8, 5, 7), (32, 3, 33), (32, 8, 16), (32, 2, 64),
            (16, 8, 16), (32, 1, 32))
-KNOBS = ("BH_FUSED_SPL", "BH_FUSED_WIDE", "BH_FUSED_WARPS", "BH_FUSED_CAP")
+KNOBS = ("BH_FUSED_SPL", "BH_FUSED_WIDE", "BH_FUSED_WARPS", "BH_FUSED_CAP", "BH_FUSED_MODE", "BH_FUSED_SMEM_TILES",
+         "BH_FUSED_GRID")
 
 
 def main():
@@ -50,15 +51,35 @@ def main():
             knobs["BH_FUSED_WARPS"] = str(int(rng.choice([1, 3, 8, 16, 24])))
         if rng.random() < 0.2:
             knobs["BH_FUSED_CAP"] = str(int(rng.choice([64, 300, 1024, 4096])))
+        if rng.random() < 0.3:
+            knobs["BH_FUSED_MODE"] = str(int(rng.integers(1, 3)))
+        if rng.random() < 0.15:
+            knobs["BH_FUSED_SMEM_TILES"] = str(int(rng.choice([0, 4, 64])))
+        if rng.random() < 0.15:
+            knobs["BH_FUSED_GRID"] = str(int(rng.choice([1, 2, 7, 40])))
         os.environ.update(knobs)
         codes = gaussian_codes(n, bins, sigma, eps, seed=int(rng.integers(1 << 31)))
-        book = ph.book_for(codes, 16)
+        import torch
+        book = ph.book_for_device(torch.from_numpy(codes.view(np.int16)).cuda(), n, 16)
+        if rng.random() < 0.2 and book.entries != ph.book_for(codes, 16).entries:
+            print(f"case {cases + 1}: device book differs from the host build_lengths", flush=True)
+            fails += 1
         st = ph.encode(codes, book, ph.LayoutConfig(*lay), with_gap=True)
+        th = int(rng.integers(1, 9))
         outs = {
             "gap": ph.gap_decoder.decode(st),
             "sync": ph.sync_decoder.decode(st),
-            "gap_tuned": ph.gap_decoder.decode(st, tuner_config=ph.TunerConfig(t_high=int(rng.integers(1, 9)))),
+            "gap_tuned": ph.gap_decoder.decode(st, tuner_config=ph.TunerConfig(t_high=th)),
+            "sync_tuned": ph.sync_decoder.decode(st, tuner_config=ph.TunerConfig(t_high=th)),
         }
+        if (lay[0] * lay[1] * lay[2]) % 128 == 0 and st.num_seqs > 2 and rng.random() < 0.5:
+            from paper_2201_09118_b200 import shard
+            world = int(rng.integers(2, 5))
+            v = "gap" if rng.random() < 0.5 else "sync"
+            parts = []
+            for r in range(world):
+                parts += [(o0, t.cpu().numpy().view(np.uint16)) for _, o0, t in shard.decode_shard([st], r, world, v)]
+            outs[f"shard{world}_{v}"] = np.concatenate([p for _, p in sorted(parts, key=lambda x: x[0])])
         bad = [k for k, v in outs.items() if not np.array_equal(v, codes)]
         cases += 1
         fails += bool(bad)
