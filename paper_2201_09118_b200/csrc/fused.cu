@@ -253,6 +253,7 @@ struct FTab {
   uint32_t dst;    // entry stride shift: 7 (8 replicas x 16 B) or 4 (16 B)
   uint32_t l12;    // shared address of lut12
   uint32_t c12;    // shared address of clut12
+  uint32_t c15;    // shared address of the 15-bit count table (phase 1 of M_WIDE3; 0 = none)
   uint32_t ljs;    // shared address of the canonical symbol order (0: read it from global)
   uint32_t lim;    // shared address of lim (u64[33])
   uint32_t base;   // shared address of base (i64[33])
@@ -319,6 +320,26 @@ __device__ __forceinline__ uint32_t clen(uint32_t win, const FTab& T) {
 // than 12 bits takes one codeword.
 __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, const FTab& T, uint32_t& n) {
   const uint32_t ct = pin(T.c12);
+  if (T.c15) {
+    // 15-bit count table (M_WIDE3 phase 1): every whole codeword of the next
+    // 15 bits per lookup, two lookups per advance; the window end and codes
+    // longer than 15 bits fall through to the 12-bit loop below
+    const uint32_t c5 = pin(T.c15);
+#pragma unroll (kUnroll)
+    while (true) {
+      const uint32_t win = r.peek();
+      const uint32_t y = lds8(c5 + (win >> (32 - C15)));
+      const uint32_t b = y >> 4;
+      if (y == 0 || pos + b > stop) break;
+      const uint32_t y2 = lds8(c5 + ((win << b) >> (32 - C15)));
+      const uint32_t b2 = y2 >> 4;
+      const bool two = y2 != 0 && pos + b + b2 <= stop;
+      n += (y & 15u) + (two ? (y2 & 15u) : 0u);
+      const uint32_t adv = b + (two ? b2 : 0u);
+      r.skip(adv);
+      pos += adv;
+    }
+  }
   while (pos < stop) {
     // tight loop: whole entries that end at or before the window end (one
     // extra lookup when an entry ends exactly at it)
@@ -1113,13 +1134,13 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     mbar_init(bar_dt, 1);
     mbar_init(bar_off, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(bar_ct, T_LIMBASE + 2 * FB_SIZE + a.ljs_bytes);
+    mbar_expect_tx(bar_ct, T_LIMBASE + 2 * FB_SIZE + a.ljs_bytes + (MODE == M_WIDE3 ? C15_SIZE : 0));
+    if (MODE == M_WIDE3) bulk_g2s(sm_s, tb_ + L.c15, C15_SIZE, bar_ct);  // decode-table region, phase 1
     bulk_g2s(sm_s + a.t_c12, tb_ + L.clut12, 2 * FB_SIZE, bar_ct);
     if (a.ljs_bytes) bulk_g2s(sm_s + a.t_ljs, tb_ + L.ljsym, a.ljs_bytes, bar_ct);
     bulk_g2s(sm_s + a.t_lim, tb_ + L.lim, T_LIMBASE, bar_ct);  // lim, base (contiguous)
     if (MODE == M_WIDE3) {
-      mbar_expect_tx(bar_dt, T_WIDE3_DEC);
-      bulk_g2s(sm_s, tb_ + L.wlut12n, T_WIDE3_DEC, bar_dt);
+      // wlut12n replaces c15 at the phase boundary (below)
     } else if (MODE == M_WIDE) {
       mbar_expect_tx(bar_dt, T_WIDE_DEC);
       bulk_g2s(sm_s, tb_ + L.wlut12, T_WIDE_DEC, bar_dt);
@@ -1148,6 +1169,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   T.base = sm_s + a.t_lim + 33 * 8;
   T.l12 = (MODE == M_NARROW && a.has_l12) ? sm_s + a.t_l12 : 0u;
   T.c12 = sm_s + a.t_c12;
+  T.c15 = MODE == M_WIDE3 ? sm_s : 0u;
   T.ljs = (a.ljs_bytes && hdr->kind == 0) ? sm_s + a.t_ljs : 0u;
   T.t = table_view(a.table, a.max_codes, hdr->ncodes);
   T.kind = hdr->kind;
@@ -1354,11 +1376,19 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
 
   // ---- tile offsets within the range, CTA aggregate -----------------------
   // wlut8 replicated 8 ways ([entry][replica] uint4) from its packed copy
-  mbar_wait(bar_dt, 0);
+  if (MODE != M_WIDE3) mbar_wait(bar_dt, 0);
   if (MODE == M_NARROW)
     for (uint32_t i = threadIdx.x; i < 256 * 8; i += blockDim.x)
       sts128(sm_s + 16 * i, lds128(sm_s + a.t_wp + 16 * (i >> 3)));
   __syncthreads();  // tile totals and the replicated decode table visible
+  if (MODE == M_WIDE3 && threadIdx.x == 0) {
+    // every warp is done with c15: the decode table takes its place
+    TableLayout L(a.max_codes);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    mbar_expect_tx(bar_dt, T_WIDE3_DEC);
+    bulk_g2s(sm_s, static_cast<const char*>(a.table) + L.wlut12n, T_WIDE3_DEC, bar_dt);
+  }
+  T.c15 = 0u;
   if (threadIdx.x == 0) {
     atomicMax(&a.rep->phase_ns[VAR == BH_VARIANT_GAP ? 2 : 1], s_tcount);
     if (VAR == BH_VARIANT_SYNC) atomicMax(&a.rep->phase_ns[2], s_tseam);
@@ -1449,6 +1479,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     if (VAR == BH_VARIANT_SYNC) dlt_n = a.tile_dlt[tile];
   }
   uint32_t dk = 0;  // tiles decoded (trace slots)
+  if (MODE == M_WIDE3) mbar_wait(bar_dt, 0);  // the decode table has replaced c15
   for (; tile < t1;) {
     const uint64_t tn = grab();
     const uint32_t info = info_n;

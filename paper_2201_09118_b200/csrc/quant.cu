@@ -141,43 +141,43 @@ __global__ void __launch_bounds__(DQ_THREADS) k_dq_reduce(const uint16_t* __rest
   }
 }
 
-// pass 2 (one CTA): exclusive segmented scan of the tile aggregates -> tile prefixes
+// pass 2 (one CTA): exclusive segmented scan of the tile aggregates -> tile
+// prefixes; every thread scans a contiguous run of tiles, the block scans the
+// run totals, and every thread rewalks its run
 __global__ void __launch_bounds__(1024) k_dq_scan(long long* __restrict__ aggs, const uint8_t* __restrict__ resets,
                                                   uint64_t ntiles) {
   __shared__ Seg s_w[32];
-  __shared__ Seg s_carry;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_carry = Seg{0, 0};
+  const uint64_t per = (ntiles + 1023) / 1024;
+  const uint64_t b0 = min((uint64_t)tid * per, ntiles), b1 = min(b0 + per, ntiles);
+  Seg t{0, 0};
+  for (uint64_t i = b0; i < b1; ++i) t = seg_op(t, Seg{aggs[i], resets[i]});
+  Seg x = t;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    Seg y{__shfl_up_sync(0xffffffffu, x.s, o), __shfl_up_sync(0xffffffffu, x.r, o)};
+    if ((int)lane >= o) x = seg_op(y, x);
+  }
+  if (lane == 31) s_w[warp] = x;
   __syncthreads();
-  for (uint64_t b0 = 0; b0 < ntiles; b0 += 1024) {
-    const uint64_t i = b0 + tid;
-    const Seg a = i < ntiles ? Seg{aggs[i], resets[i]} : Seg{0, 0};
-    Seg x = a;
+  if (warp == 0) {
+    Seg z = s_w[lane];
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      Seg y{__shfl_up_sync(0xffffffffu, x.s, o), __shfl_up_sync(0xffffffffu, x.r, o)};
-      if ((int)lane >= o) x = seg_op(y, x);
+      Seg y{__shfl_up_sync(0xffffffffu, z.s, o), __shfl_up_sync(0xffffffffu, z.r, o)};
+      if ((int)lane >= o) z = seg_op(y, z);
     }
-    if (lane == 31) s_w[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      Seg z = s_w[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        Seg y{__shfl_up_sync(0xffffffffu, z.s, o), __shfl_up_sync(0xffffffffu, z.r, o)};
-        if ((int)lane >= o) z = seg_op(y, z);
-      }
-      s_w[lane] = z;
-    }
-    __syncthreads();
-    Seg pre = s_carry;
-    if (warp) pre = seg_op(pre, s_w[warp - 1]);
-    const Seg lp{__shfl_up_sync(0xffffffffu, x.s, 1), __shfl_up_sync(0xffffffffu, x.r, 1)};
-    if (lane) pre = seg_op(pre, lp);
-    if (i < ntiles) aggs[i] = pre.s;  // exclusive prefix (the running value before the tile)
-    __syncthreads();
-    if (tid == 0) s_carry = seg_op(s_carry, s_w[31]);
-    __syncthreads();
+    s_w[lane] = z;
+  }
+  __syncthreads();
+  Seg pre{0, 0};
+  if (warp) pre = s_w[warp - 1];
+  const Seg lp{__shfl_up_sync(0xffffffffu, x.s, 1), __shfl_up_sync(0xffffffffu, x.r, 1)};
+  if (lane) pre = seg_op(pre, lp);
+  for (uint64_t i = b0; i < b1; ++i) {
+    const Seg a{aggs[i], resets[i]};
+    aggs[i] = pre.s;  // exclusive prefix: the running value before tile i
+    pre = seg_op(pre, a);
   }
 }
 
@@ -206,15 +206,23 @@ __global__ void __launch_bounds__(DQ_THREADS) k_dequant(const uint16_t* __restri
     r[k] = (double)run * twice_eb;  // exact: |run| < 2^24, twice_eb a power of two
   }
   if (bad) w->inexact = 1;
-  const uint64_t i0 = (uint64_t)blockIdx.x * DQ_TILE + (uint64_t)threadIdx.x * DQ_ITEMS;
-  if (i0 + DQ_ITEMS <= n) {
-    double2* dst = reinterpret_cast<double2*>(out + i0);
+  // through shared memory (rows of 16 padded to 17 doubles: conflict-free),
+  // so each warp store covers 512 consecutive bytes
+  extern __shared__ double s_out[];
 #pragma unroll
-    for (int k = 0; k < DQ_ITEMS / 2; ++k) dst[k] = make_double2(r[2 * k], r[2 * k + 1]);
-  } else {
+  for (int k = 0; k < DQ_ITEMS; ++k) s_out[threadIdx.x * (DQ_ITEMS + 1) + k] = r[k];
+  __syncthreads();
+  const uint64_t t0 = (uint64_t)blockIdx.x * DQ_TILE;
 #pragma unroll
-    for (int k = 0; k < DQ_ITEMS; ++k)
-      if (i0 + k < n) out[i0 + k] = r[k];
+  for (int j = 0; j < DQ_ITEMS / 2; ++j) {
+    const uint32_t q = (uint32_t)j * 2 * DQ_THREADS + 2 * threadIdx.x;  // item pair within the tile
+    const uint32_t sa = (q / DQ_ITEMS) * (DQ_ITEMS + 1) + (q % DQ_ITEMS);
+    const uint64_t g = t0 + q;
+    if (g + 2 <= n) {
+      *reinterpret_cast<double2*>(out + g) = make_double2(s_out[sa], s_out[sa + 1]);
+    } else if (g < n) {
+      out[g] = s_out[sa];
+    }
   }
 }
 
@@ -285,8 +293,8 @@ extern "C" int bh_dequantize(const uint16_t* codes_dev, uint64_t n, const int64_
       k_dq_reduce<<<(unsigned)nt, DQ_THREADS, 0, st>>>(codes_dev, n, outlier_idx_dev, un, n_outliers,
                                                        (int32_t)midpoint, aggs, resets, w);
       k_dq_scan<<<1, 1024, 0, st>>>(aggs, resets, nt);
-      k_dequant<<<(unsigned)nt, DQ_THREADS, 0, st>>>(codes_dev, n, outlier_idx_dev, un, n_outliers, twice_eb,
-                                                     (int32_t)midpoint, aggs, out_dev, w);
+      k_dequant<<<(unsigned)nt, DQ_THREADS, DQ_THREADS * (DQ_ITEMS + 1) * sizeof(double), st>>>(
+          codes_dev, n, outlier_idx_dev, un, n_outliers, twice_eb, (int32_t)midpoint, aggs, out_dev, w);
     }
     if (cudaMemcpyAsync(inexact_dev, &w->inexact, 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       return BH_CUDA_ERROR;

@@ -256,6 +256,19 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
     wlut12[v] = wl;
     wlut12n[v] = narrow3(sy[0], sy[1], sy[2], v, s_l12);
   }
+  uint8_t* c15 = reinterpret_cast<uint8_t*>(reinterpret_cast<char*>(blob) + L.c15);
+  for (int v = threadIdx.x; v < C15_SIZE; v += blockDim.x) {
+    const uint32_t w0 = (uint32_t)v << (32 - C15);
+    uint32_t pos = 0, n = 0;
+    while (pos < (uint32_t)C15) {
+      uint32_t len = (s_l12[(w0 << pos) >> (32 - FB)] >> 16) & 0xffu;
+      if (!len) len = (slow_lookup(t, w0 << pos) >> 16) & 0xffu;
+      if (len == 0 || pos + len > (uint32_t)C15) break;
+      pos += len;
+      ++n;
+    }
+    c15[v] = (uint8_t)(n | (pos << 4));
+  }
   uint16_t* s_len12 = reinterpret_cast<uint16_t*>(s_lut);  // 4096 lengths (8 KB)
   for (int v = threadIdx.x; v < FB_SIZE; v += blockDim.x) s_len12[v] = (uint16_t)((s_l12[v] >> 16) & 0xff);
   __syncthreads();
@@ -478,6 +491,21 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   uint8_t* clut8 = reinterpret_cast<uint8_t*>(B + L.clut8);
   uint4* wlut8 = reinterpret_cast<uint4*>(B + L.wlut8);
   constexpr uint32_t N12 = FB_SIZE, N11 = LUT_SIZE, N8 = 256;
+  // 15-bit count table (whole codewords of the window): codes up to 12 bits
+  // from the prefix table, longer ones by the limit search
+  uint8_t* c15 = reinterpret_cast<uint8_t*>(B + L.c15);
+  for (uint32_t v = cta * K1_THREADS + tid; v < (uint32_t)C15_SIZE; v += G * K1_THREADS) {
+    const uint32_t w0 = v << (32 - C15);
+    uint32_t pos = 0, n = 0;
+    while (pos < (uint32_t)C15) {
+      uint32_t len = (S.l12[(w0 << pos) >> (32 - FB)] >> 16) & 0xffu;
+      if (!len) len = (canon_one(S, w0 << pos) >> 16) & 0xffu;  // > 12 bits (or no codeword)
+      if (len == 0 || pos + len > (uint32_t)C15) break;
+      pos += len;
+      ++n;
+    }
+    c15[v] = (uint8_t)(n | (pos << 4));
+  }
   for (uint32_t it = cta * K1_THREADS + tid; it < N12 + N11 + N8; it += G * K1_THREADS) {
     const uint32_t W = it < N12 ? (uint32_t)FB : it < N12 + N11 ? (uint32_t)LUT_BITS : 8u;
     const uint32_t v = it < N12 ? it : it < N12 + N11 ? it - N12 : it - N12 - N11;

@@ -254,7 +254,10 @@ def ingest_shard(path, rank: int = 0, world: int = 1, variant: str = "gap", devi
     cap = tb // max(book.min_len, 1) + 1  # codewords starting in the span
     c = _lib.Stream(words.data_ptr(), tb, cap, sb, sps, book.symbol_width, max_codes, gap_d.data_ptr(),
                     table.data_ptr(), int(g[0]) if s0 else 0, _lib.STREAM_COUNT_IS_CAPACITY)
-    var = _lib.VARIANT_GAP if variant == "gap" else _lib.VARIANT_SYNC
+    from .shard import kraft_complete
+    # incomplete books: the fused self-sync kernel declines them and a chunk
+    # has no staged fallback -- enter through the gap bytes (same symbols)
+    var = _lib.VARIANT_SYNC if variant != "gap" and kraft_complete(book) else _lib.VARIANT_GAP
     tune = make_tune(max_len=book.max_len, min_len=book.min_len)
     out = empty(cap, np.uint16, dev)
     n = 0

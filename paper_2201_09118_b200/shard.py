@@ -173,6 +173,11 @@ def piece_chunk(total_bits: int, subseq_bits: int, subseqs_per_seq: int, gap, su
     return _chunk(q0, q1, total_bits, subseq_bits, subseqs_per_seq, gap, oi)
 
 
+def kraft_complete(book) -> bool:
+    """Kraft sum exactly 1 (every bit pattern decodes)."""
+    return sum(1 << (32 - ln) for _, ln in book.entries.values()) == 1 << 32
+
+
 def decode_shard(streams, rank: int = 0, world: int = 1, variant: str = "gap", device=None):
     """Decode this rank's share of a batch of streams (BASELINE
     config 5): the batch's sequences cut into `world` equal contiguous spans
@@ -194,7 +199,6 @@ def decode_shard(streams, rank: int = 0, world: int = 1, variant: str = "gap", d
     from .gap_decoder import count_pass, entries_from_gap
     from .errors import NotPresent
     lib = _lib.load()
-    var = _lib.VARIANT_GAP if variant == "gap" else _lib.VARIANT_SYNC
     for st in streams:
         if st.gap is None:
             raise NotPresent("sharded decode needs every stream's gap array")
@@ -224,6 +228,12 @@ def decode_shard(streams, rank: int = 0, world: int = 1, variant: str = "gap", d
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
     results, keep = [], []
     for k, (fi, out0, n, tb, c, book) in enumerate(plan):
+        # the self-sync decoder's fused kernel declines incomplete books (a
+        # single-symbol book) and a chunk cannot take the staged
+        # pipeline: such pieces are entered through their gap bytes instead
+        # (same symbols -- the synchronised state is the unique fixpoint)
+        sync_ok = variant != "gap" and kraft_complete(book)
+        var = _lib.VARIANT_SYNC if sync_ok else _lib.VARIANT_GAP
         tune = make_tune(max_len=book.max_len, min_len=book.min_len)
         if len(plan) > 1:
             tune.ctas = max(1, round(sms * tb / max(total_bits, 1)))

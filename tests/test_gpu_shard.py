@@ -55,3 +55,21 @@ def test_chunked_decode_matches_whole_stream(ph, sigma, n, variant, nchunks):
         check(rep.read().status, "chunk")
         got[ch.out0:ch.out0 + ch.n] = out[:ch.n].cpu().numpy().view(np.uint16)
     assert np.array_equal(got, codes)
+
+
+@pytest.mark.parametrize("variant", ["gap", "sync"])
+def test_decode_shard_single_symbol_book(variant):
+    """A single-symbol book is incomplete (Kraft 1/2): the self-sync fused
+    kernel declines it and a chunk has no staged fallback, so decode_shard
+    enters such pieces through their gap bytes -- same symbols."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_09118_b200 as ph
+    from paper_2201_09118_b200 import shard
+    codes = np.full(300_000, 7, np.uint16)
+    st = ph.encode(codes, ph.book_for(codes, 16), ph.DEFAULT_LAYOUT, with_gap=True)
+    for world in (1, 3):
+        parts = sorted((o0, t.cpu().numpy().view(np.uint16)) for r in range(world)
+                       for _, o0, t in shard.decode_shard([st], r, world, variant))
+        assert np.array_equal(np.concatenate([p for _, p in parts]), codes)
