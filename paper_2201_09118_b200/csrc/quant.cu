@@ -151,7 +151,17 @@ __global__ void __launch_bounds__(1024) k_dq_scan(long long* __restrict__ aggs, 
   const uint64_t per = (ntiles + 1023) / 1024;
   const uint64_t b0 = min((uint64_t)tid * per, ntiles), b1 = min(b0 + per, ntiles);
   Seg t{0, 0};
-  for (uint64_t i = b0; i < b1; ++i) t = seg_op(t, Seg{aggs[i], resets[i]});
+  for (uint64_t i = b0; i < b1; i += 8) {  // batches of loads in flight
+    long long av[8];
+    uint8_t rv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      av[k] = i + k < b1 ? aggs[i + k] : 0ll;
+      rv[k] = i + k < b1 ? resets[i + k] : (uint8_t)0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t = seg_op(t, Seg{av[k], rv[k]});
+  }
   Seg x = t;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -174,10 +184,50 @@ __global__ void __launch_bounds__(1024) k_dq_scan(long long* __restrict__ aggs, 
   if (warp) pre = s_w[warp - 1];
   const Seg lp{__shfl_up_sync(0xffffffffu, x.s, 1), __shfl_up_sync(0xffffffffu, x.r, 1)};
   if (lane) pre = seg_op(pre, lp);
-  for (uint64_t i = b0; i < b1; ++i) {
-    const Seg a{aggs[i], resets[i]};
-    aggs[i] = pre.s;  // exclusive prefix: the running value before tile i
-    pre = seg_op(pre, a);
+  for (uint64_t i = b0; i < b1; i += 8) {
+    long long av[8];
+    uint8_t rv[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      av[k] = i + k < b1 ? aggs[i + k] : 0ll;
+      rv[k] = i + k < b1 ? resets[i + k] : (uint8_t)0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      if (i + k < b1) aggs[i + k] = pre.s;  // exclusive prefix: the running value before tile i+k
+      pre = seg_op(pre, Seg{av[k], rv[k]});
+    }
+  }
+}
+
+// pass 1 without outliers: each tile's sum of (code - midpoint), lean enough
+// for eight CTAs per SM (bytes in flight)
+__global__ void __launch_bounds__(DQ_THREADS) k_dq_reduce_plain(const uint16_t* __restrict__ codes, uint64_t n,
+                                                                int32_t mid, long long* __restrict__ aggs,
+                                                                uint8_t* __restrict__ resets) {
+  __shared__ long long s_w[DQ_THREADS / 32];
+  const uint64_t i0 = (uint64_t)blockIdx.x * DQ_TILE + (uint64_t)threadIdx.x * DQ_ITEMS;
+  long long acc = 0;
+  if (i0 + DQ_ITEMS <= n) {
+    const uint4* src = reinterpret_cast<const uint4*>(codes + i0);
+    const uint4 a = __ldg(src), b = __ldg(src + 1);
+    uint32_t sm = 0;
+    const uint32_t wv[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+    for (int k = 0; k < 8; ++k) sm += (wv[k] & 0xffffu) + (wv[k] >> 16);
+    acc = (long long)sm - (long long)DQ_ITEMS * mid;
+  } else {
+    for (uint64_t i = i0; i < n && i < i0 + DQ_ITEMS; ++i) acc += (long long)codes[i] - mid;
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) s_w[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    long long t = 0;
+#pragma unroll
+    for (int w = 0; w < DQ_THREADS / 32; ++w) t += s_w[w];
+    aggs[blockIdx.x] = t;
+    resets[blockIdx.x] = 0;
   }
 }
 
@@ -290,8 +340,11 @@ extern "C" int bh_dequantize(const uint16_t* codes_dev, uint64_t n, const int64_
     if (n) {
       // reduce -> scan of the tile aggregates -> apply: every pass streams at
       // HBM speed with no inter-CTA waiting (12 B per code in all)
-      k_dq_reduce<<<(unsigned)nt, DQ_THREADS, 0, st>>>(codes_dev, n, outlier_idx_dev, un, n_outliers,
-                                                       (int32_t)midpoint, aggs, resets, w);
+      if (n_outliers)
+        k_dq_reduce<<<(unsigned)nt, DQ_THREADS, 0, st>>>(codes_dev, n, outlier_idx_dev, un, n_outliers,
+                                                         (int32_t)midpoint, aggs, resets, w);
+      else
+        k_dq_reduce_plain<<<(unsigned)nt, DQ_THREADS, 0, st>>>(codes_dev, n, (int32_t)midpoint, aggs, resets);
       k_dq_scan<<<1, 1024, 0, st>>>(aggs, resets, nt);
       k_dequant<<<(unsigned)nt, DQ_THREADS, DQ_THREADS * (DQ_ITEMS + 1) * sizeof(double), st>>>(
           codes_dev, n, outlier_idx_dev, un, n_outliers, twice_eb, (int32_t)midpoint, aggs, out_dev, w);

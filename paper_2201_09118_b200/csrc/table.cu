@@ -257,10 +257,16 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
     wlut12n[v] = narrow3(sy[0], sy[1], sy[2], v, s_l12);
   }
   uint8_t* c15 = reinterpret_cast<uint8_t*>(reinterpret_cast<char*>(blob) + L.c15);
+  __shared__ uint32_t s_minl;
+  if (threadIdx.x == 0) s_minl = 64;
+  __syncthreads();
+  for (uint32_t i = threadIdx.x; i < t.ncodes; i += blockDim.x) atomicMin(&s_minl, (uint32_t)t.ljlen[i]);
+  __syncthreads();
+  const bool build15 = s_minl >= 4 && s_minl != 64;
   for (int v = threadIdx.x; v < C15_SIZE; v += blockDim.x) {
     const uint32_t w0 = (uint32_t)v << (32 - C15);
     uint32_t pos = 0, n = 0;
-    while (pos < (uint32_t)C15) {
+    while (build15 && pos < (uint32_t)C15) {
       uint32_t len = (s_l12[(w0 << pos) >> (32 - FB)] >> 16) & 0xffu;
       if (!len) len = (slow_lookup(t, w0 << pos) >> 16) & 0xffu;
       if (len == 0 || pos + len > (uint32_t)C15) break;
@@ -338,6 +344,7 @@ struct CanonSmem {
   uint32_t wcnt[K1_THREADS / 32][33];
   uint32_t wpre[K1_THREADS / 32][33];
   uint16_t sym[FB_SIZE];  // canonical order of the codes of length <= 12
+  uint32_t minl;          // shortest code length
   uint32_t l12[FB_SIZE];  // sym | len<<16 of the codeword at each 12-bit prefix (codes <= 12 bits)
   int bad;
 };
@@ -403,6 +410,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
     const unsigned used = __ballot_sync(0xffffffffu, c != 0);
     const uint32_t ml = used ? 32 - __clz(used) : 0;
     if (lane == 0) {
+      S.minl = used ? __ffs(used) : 0;
       S.lim[0] = 0;
       S.base[0] = 0;
       if (ncodes > max_codes) S.bad = 1;
@@ -493,11 +501,15 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   constexpr uint32_t N12 = FB_SIZE, N11 = LUT_SIZE, N8 = 256;
   // 15-bit count table (whole codewords of the window): codes up to 12 bits
   // from the prefix table, longer ones by the limit search
+  // (built for books whose codes are all >= 4 bits -- the only ones the
+  // fused kernel counts with it -- and all zero, "use the 12-bit table",
+  // otherwise)
   uint8_t* c15 = reinterpret_cast<uint8_t*>(B + L.c15);
+  const bool build15 = S.minl >= 4;
   for (uint32_t v = cta * K1_THREADS + tid; v < (uint32_t)C15_SIZE; v += G * K1_THREADS) {
     const uint32_t w0 = v << (32 - C15);
     uint32_t pos = 0, n = 0;
-    while (pos < (uint32_t)C15) {
+    while (build15 && pos < (uint32_t)C15) {
       uint32_t len = (S.l12[(w0 << pos) >> (32 - FB)] >> 16) & 0xffu;
       if (!len) len = (canon_one(S, w0 << pos) >> 16) & 0xffu;  // > 12 bits (or no codeword)
       if (len == 0 || pos + len > (uint32_t)C15) break;

@@ -32,7 +32,8 @@ def layout(max_codes: int) -> dict:
     L["clut12"] = L["lut12"] + 4 * 4096
     L["wlut12"] = a16(L["clut12"] + 2 * 4096)
     L["wlut12n"] = a16(L["wlut12"] + 16 * 4096)
-    L["lim"] = a16(L["wlut12n"] + 8 * 4096)
+    L["c15"] = a16(L["wlut12n"] + 8 * 4096)
+    L["lim"] = a16(L["c15"] + 32768)
     L["base"] = L["lim"] + 8 * 33
     L["lj"] = a16(L["base"] + 8 * 33)
     L["ljsym"] = a16(L["lj"] + 4 * max_codes)
@@ -85,9 +86,10 @@ def test_canonical_tables_match_general_builder(env):
         assert np.array_equal(hf[1:7], hg[1:7]), (hf[:7], hg[:7])  # max_len ncodes lut_bits alphabet status complete
         ncodes = int(hf[2])
         assert ncodes == len(book.entries)
-        for name in ("lut", "cnt", "dlut8", "clut8", "wlut8", "lut12", "clut12", "wlut12", "wlut12n"):
+        for name in ("lut", "cnt", "dlut8", "clut8", "wlut8", "lut12", "clut12", "wlut12", "wlut12n", "c15"):
             nxt = {"lut": "cnt", "cnt": "dlut8", "dlut8": "clut8", "clut8": "wlut8", "wlut8": "lut12",
-                   "lut12": "clut12", "clut12": "wlut12", "wlut12": "wlut12n", "wlut12n": "lim"}[name]
+                   "lut12": "clut12", "clut12": "wlut12", "wlut12": "wlut12n", "wlut12n": "c15",
+                   "c15": "lim"}[name]
             assert np.array_equal(f[L[name]:L[nxt]], g[L[name]:L[nxt]]), (name, book.max_len, ncodes)
         for name, w in (("lj", 4), ("ljsym", 2), ("ljlen", 1)):
             assert np.array_equal(f[L[name]:L[name] + w * ncodes], g[L[name]:L[name] + w * ncodes]), name
@@ -98,3 +100,48 @@ def test_canonical_tables_match_general_builder(env):
         for ln in range(1, 33):
             assert int(lim[ln]) == (code + int(counts[ln])) << (32 - ln)
             code = (code + int(counts[ln])) << 1
+
+
+def test_count15_table_semantics(env):
+    """c15 (15-bit count table of the long-code path): for a book with every
+    code >= 4 bits, entry v = (whole codewords of the zero-filled 15-bit
+    window v) | (their end) << 4, checked against a host walk of the
+    canonical codes; all zero for books with shorter codes."""
+    torch, ph, _lib = env
+    lib = _lib.load()
+    st = torch.cuda.current_stream().cuda_stream
+    rng = np.random.default_rng(3)
+    for sigma, want_built in ((8.0, True), (22.0, True), (0.6, False)):
+        codes = np.clip(np.rint(rng.normal(0, sigma, 300_000)) + 512, 0, 1023).astype(np.uint16)
+        book = ph.book_for(codes, 16)
+        assert (book.min_len >= 4) == want_built
+        mc = len(book.entries)
+        L = layout(mc)
+        lens = book.length_bytes()
+        tab = torch.zeros(L["total"], dtype=torch.uint8, device="cuda")
+        _lib.check(lib.bh_table_build(torch.from_numpy(lens.copy()).cuda().data_ptr(), len(lens), tab.data_ptr(), mc, st))
+        c15 = tab[L["c15"]:L["c15"] + 32768].cpu().numpy()
+        if not want_built:
+            assert not c15.any()
+            continue
+        # host: left-justified code -> length, by the canonical limits
+        left = sorted(((code << (32 - ln)), ln) for code, ln in book.entries.values())
+        import bisect
+        keys = [k for k, _ in left]
+
+        def length_at(w):  # codeword length at the front of 32-bit window w (0: none)
+            i = bisect.bisect_right(keys, w) - 1
+            if i < 0:
+                return 0
+            k, ln = left[i]
+            return ln if (w ^ k) >> (32 - ln) == 0 else 0
+        for v in list(range(0, 32768, 97)) + [0, 32767, 12345]:
+            w0 = v << 17
+            pos = n = 0
+            while pos < 15:
+                ln = length_at((w0 << pos) & 0xffffffff)
+                if ln == 0 or pos + ln > 15:
+                    break
+                pos += ln
+                n += 1
+            assert c15[v] == (n | (pos << 4)), (sigma, v, c15[v], n, pos)
