@@ -70,6 +70,8 @@ struct TableHdr {
 //   c15   u8[32768]  next 15 bits -> n | bits<<4 over every whole codeword of the
 //                    window (n, bits <= 15); 0 if the first one is longer
 //                    (the count phase of the long-code fused decoders)
+//   len12 u8[4096]   next 12 bits -> length of the first codeword if <= 12 bits, else 0
+//                    (the self-sync decoders' per-codeword resynchronization walk)
 //   clut12 u16[4096] next 12 bits -> starts | bits<<12 over every whole codeword
 //                    inside the 12 bits (count pass): bit i of `starts` is set
 //                    when a codeword starts at offset i, `bits` is where the
@@ -86,7 +88,7 @@ constexpr int C15_SIZE = 1 << C15;
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct TableLayout {
-  size_t lut, cnt, dlut8, clut8, wlut8, lut12, clut12, wlut12, wlut12n, c15, lim, base, lj, ljsym, ljlen, total;
+  size_t lut, cnt, dlut8, clut8, wlut8, lut12, clut12, wlut12, wlut12n, c15, len12, lim, base, lj, ljsym, ljlen, total;
   __host__ __device__ explicit TableLayout(uint32_t max_codes) {
     lut = TABLE_HDR_BYTES;
     cnt = lut + sizeof(uint32_t) * LUT_SIZE;
@@ -98,7 +100,8 @@ struct TableLayout {
     wlut12 = align16(clut12 + 2 * (size_t)FB_SIZE);
     wlut12n = align16(wlut12 + 16 * (size_t)FB_SIZE);
     c15 = align16(wlut12n + 8 * (size_t)FB_SIZE);
-    lim = align16(c15 + (size_t)C15_SIZE);
+    len12 = align16(c15 + (size_t)C15_SIZE);
+    lim = align16(len12 + (size_t)FB_SIZE);
     base = lim + 8 * 33;
     lj = align16(base + 8 * 33);
     ljsym = align16(lj + sizeof(uint32_t) * (size_t)max_codes);

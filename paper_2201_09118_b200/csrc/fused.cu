@@ -110,6 +110,7 @@ struct FusedArgs {
   uint32_t wide;         // table layout: 1 = wlut12, 0 = replicated wlut8 (+ lut12 if has_l12)
   uint32_t t_lim, t_c12, t_wp, t_l12;  // shared-memory table offsets (bytes)
   uint32_t t_ljs, ljs_bytes;            // shared copy of ljsym for the limit search (0 bytes: global)
+  uint32_t t_len;                       // len12 (wide modes)
   uint32_t smem_tiles;                  // ranges up to this many tiles keep their totals in shared memory
   // online tuner (tuner.py:117-191): 0 = off; else per-tile class -> staging
   // window, and the per-sequence class histogram of tuner.plan
@@ -254,6 +255,7 @@ struct FTab {
   uint32_t l12;    // shared address of lut12
   uint32_t c12;    // shared address of clut12
   uint32_t c15;    // shared address of the 15-bit count table (phase 1 of M_WIDE3; 0 = none)
+  uint32_t len12;  // shared address of len12 (wide modes: first codeword length, resync walk)
   uint32_t ljs;    // shared address of the canonical symbol order (0: read it from global)
   uint32_t lim;    // shared address of lim (u64[33])
   uint32_t base;   // shared address of base (i64[33])
@@ -305,11 +307,8 @@ __device__ __forceinline__ uint32_t fone(uint32_t win, const FTab& T) {
 // length of one codeword from the 12-bit count table (second start, or the end
 // of the only whole codeword); codes longer than 12 bits take the limit search
 __device__ __forceinline__ uint32_t clen(uint32_t win, const FTab& T) {
-  const uint32_t y = lds16(T.c12 + ((win >> (32 - FB)) << 1));
-  if (y) {
-    const uint32_t m = y & 0xffeu;
-    return m ? __ffs(m) - 1 : (y >> 12);
-  }
+  const uint32_t l = lds8(T.len12 + (win >> (32 - FB)));
+  if (l) return l;
   return (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
 }
 
@@ -1134,7 +1133,9 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     mbar_init(bar_dt, 1);
     mbar_init(bar_off, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(bar_ct, T_LIMBASE + 2 * FB_SIZE + a.ljs_bytes + (MODE == M_WIDE3 ? C15_SIZE : 0));
+    mbar_expect_tx(bar_ct, T_LIMBASE + 2 * FB_SIZE + a.ljs_bytes + (MODE == M_WIDE3 ? C15_SIZE : 0) +
+                               (MODE != M_NARROW ? FB_SIZE : 0));
+    if (MODE != M_NARROW) bulk_g2s(sm_s + a.t_len, tb_ + L.len12, FB_SIZE, bar_ct);
     if (MODE == M_WIDE3) bulk_g2s(sm_s, tb_ + L.c15, C15_SIZE, bar_ct);  // decode-table region, phase 1
     bulk_g2s(sm_s + a.t_c12, tb_ + L.clut12, 2 * FB_SIZE, bar_ct);
     if (a.ljs_bytes) bulk_g2s(sm_s + a.t_ljs, tb_ + L.ljsym, a.ljs_bytes, bar_ct);
@@ -1170,6 +1171,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   T.l12 = (MODE == M_NARROW && a.has_l12) ? sm_s + a.t_l12 : 0u;
   T.c12 = sm_s + a.t_c12;
   T.c15 = MODE == M_WIDE3 ? sm_s : 0u;
+  T.len12 = sm_s + a.t_len;
   T.ljs = (a.ljs_bytes && hdr->kind == 0) ? sm_s + a.t_ljs : 0u;
   T.t = table_view(a.table, a.max_codes, hdr->ncodes);
   T.kind = hdr->kind;
@@ -1670,7 +1672,8 @@ inline uint64_t nseq_of(const bh_stream* s) { return (vnsub_of(s) + TILE_SUBSEQ 
 
 
 struct FusedCfg {
-  uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12, wide, mode, t_lim, t_c12, t_wp, t_l12, t_ljs, ljs_bytes;
+  uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12, wide, mode, t_lim, t_c12, t_wp, t_l12, t_ljs, ljs_bytes,
+      t_len;
 };
 
 FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
@@ -1705,12 +1708,14 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
     c.t_lim = c.mode == M_WIDE3 ? T_WIDE3_DEC : T_WIDE_DEC;
     c.t_c12 = c.t_lim + T_LIMBASE;
     c.t_wp = c.t_l12 = 0;
-    c.tables = (uint32_t)align16(c.t_c12 + 2 * FB_SIZE);
+    c.t_len = c.t_c12 + 2 * FB_SIZE;
+    c.tables = (uint32_t)align16(c.t_len + FB_SIZE);
   } else {
     c.t_lim = T_NARROW_DEC;
     c.t_c12 = c.t_lim + T_LIMBASE;
     c.t_wp = c.t_c12 + 2 * FB_SIZE;
     c.t_l12 = c.t_wp + 4096;
+    c.t_len = 0;
     c.tables = (uint32_t)align16(c.t_l12 + (c.has_l12 ? 4 * FB_SIZE : 0));
   }
   // codes longer than the tables reach: the canonical symbol order in shared
@@ -1859,6 +1864,7 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.t_l12 = cfg.t_l12;
   a.t_ljs = cfg.t_ljs;
   a.ljs_bytes = cfg.ljs_bytes;
+  a.t_len = cfg.t_len;
   a.t_high = 0;
   a.lanes_per_seq = 0;
   if (tuned(tune)) {

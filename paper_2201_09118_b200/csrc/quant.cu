@@ -142,61 +142,60 @@ __global__ void __launch_bounds__(DQ_THREADS) k_dq_reduce(const uint16_t* __rest
 }
 
 // pass 2 (one CTA): exclusive segmented scan of the tile aggregates -> tile
-// prefixes; every thread scans a contiguous run of tiles, the block scans the
-// run totals, and every thread rewalks its run
+// prefixes, 4096 aggregates at a time: coalesced loads into shared memory,
+// each thread scans 4 consecutive ones, the block scans the thread totals,
+// coalesced stores back (a carry links the chunks)
+constexpr int SCAN_ITEMS = 4;  // 4096 aggregates (36 KB of shared memory) per chunk
 __global__ void __launch_bounds__(1024) k_dq_scan(long long* __restrict__ aggs, const uint8_t* __restrict__ resets,
                                                   uint64_t ntiles) {
+  __shared__ long long s_v[1024 * SCAN_ITEMS];
+  __shared__ uint8_t s_r[1024 * SCAN_ITEMS];
   __shared__ Seg s_w[32];
+  __shared__ Seg s_carry;
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint64_t per = (ntiles + 1023) / 1024;
-  const uint64_t b0 = min((uint64_t)tid * per, ntiles), b1 = min(b0 + per, ntiles);
-  Seg t{0, 0};
-  for (uint64_t i = b0; i < b1; i += 8) {  // batches of loads in flight
-    long long av[8];
-    uint8_t rv[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      av[k] = i + k < b1 ? aggs[i + k] : 0ll;
-      rv[k] = i + k < b1 ? resets[i + k] : (uint8_t)0;
+  if (tid == 0) s_carry = Seg{0, 0};
+  for (uint64_t c0 = 0; c0 < ntiles; c0 += 1024 * SCAN_ITEMS) {
+    const uint32_t m = (uint32_t)min((uint64_t)1024 * SCAN_ITEMS, ntiles - c0);
+    for (uint32_t i = tid; i < 1024 * SCAN_ITEMS; i += 1024) {
+      s_v[i] = i < m ? aggs[c0 + i] : 0ll;
+      s_r[i] = i < m ? resets[c0 + i] : (uint8_t)0;
     }
+    __syncthreads();
+    Seg t{0, 0};
 #pragma unroll
-    for (int k = 0; k < 8; ++k) t = seg_op(t, Seg{av[k], rv[k]});
-  }
-  Seg x = t;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    Seg y{__shfl_up_sync(0xffffffffu, x.s, o), __shfl_up_sync(0xffffffffu, x.r, o)};
-    if ((int)lane >= o) x = seg_op(y, x);
-  }
-  if (lane == 31) s_w[warp] = x;
-  __syncthreads();
-  if (warp == 0) {
-    Seg z = s_w[lane];
+    for (int k = 0; k < SCAN_ITEMS; ++k) t = seg_op(t, Seg{s_v[tid * SCAN_ITEMS + k], s_r[tid * SCAN_ITEMS + k]});
+    Seg x = t;
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      Seg y{__shfl_up_sync(0xffffffffu, z.s, o), __shfl_up_sync(0xffffffffu, z.r, o)};
-      if ((int)lane >= o) z = seg_op(y, z);
+      Seg y{__shfl_up_sync(0xffffffffu, x.s, o), __shfl_up_sync(0xffffffffu, x.r, o)};
+      if ((int)lane >= o) x = seg_op(y, x);
     }
-    s_w[lane] = z;
-  }
-  __syncthreads();
-  Seg pre{0, 0};
-  if (warp) pre = s_w[warp - 1];
-  const Seg lp{__shfl_up_sync(0xffffffffu, x.s, 1), __shfl_up_sync(0xffffffffu, x.r, 1)};
-  if (lane) pre = seg_op(pre, lp);
-  for (uint64_t i = b0; i < b1; i += 8) {
-    long long av[8];
-    uint8_t rv[8];
+    if (lane == 31) s_w[warp] = x;
+    __syncthreads();
+    if (warp == 0) {
+      Seg z = s_w[lane];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      av[k] = i + k < b1 ? aggs[i + k] : 0ll;
-      rv[k] = i + k < b1 ? resets[i + k] : (uint8_t)0;
+      for (int o = 1; o < 32; o <<= 1) {
+        Seg y{__shfl_up_sync(0xffffffffu, z.s, o), __shfl_up_sync(0xffffffffu, z.r, o)};
+        if ((int)lane >= o) z = seg_op(y, z);
+      }
+      s_w[lane] = z;
     }
+    __syncthreads();
+    Seg pre = s_carry;
+    if (warp) pre = seg_op(pre, s_w[warp - 1]);
+    const Seg lp{__shfl_up_sync(0xffffffffu, x.s, 1), __shfl_up_sync(0xffffffffu, x.r, 1)};
+    if (lane) pre = seg_op(pre, lp);
 #pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      if (i + k < b1) aggs[i + k] = pre.s;  // exclusive prefix: the running value before tile i+k
-      pre = seg_op(pre, Seg{av[k], rv[k]});
+    for (int k = 0; k < SCAN_ITEMS; ++k) {
+      const Seg a{s_v[tid * SCAN_ITEMS + k], s_r[tid * SCAN_ITEMS + k]};
+      s_v[tid * SCAN_ITEMS + k] = pre.s;  // exclusive prefix: the running value before the tile
+      pre = seg_op(pre, a);
     }
+    __syncthreads();
+    for (uint32_t i = tid; i < m; i += 1024) aggs[c0 + i] = s_v[i];
+    if (tid == 0) s_carry = seg_op(s_carry, s_w[31]);
+    __syncthreads();
   }
 }
 

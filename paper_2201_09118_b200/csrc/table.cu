@@ -233,6 +233,7 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
     const uint32_t len = (e >> 16) & 0xff;
     lut12[v] = len <= (uint32_t)FB ? e : 0u;
     s_l12[v] = len <= (uint32_t)FB ? e : 0u;
+    reinterpret_cast<uint8_t*>(reinterpret_cast<char*>(blob) + L.len12)[v] = (uint8_t)(len <= (uint32_t)FB ? len : 0u);
   }
   __syncthreads();
   // up to six whole codewords of the 12-bit window (wide decode table)
@@ -547,6 +548,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
     wl.z = sz;
     if (it < N12) {
       lut12[v] = first;
+      reinterpret_cast<uint8_t*>(B + L.len12)[v] = (uint8_t)((first >> 16) & 0xffu);
       clut12[v] = (uint16_t)(starts | (pos << 12));
       wl.w = n6 ? (p6 | (n6 << 4) | (l0 << 16) | ((2 * n6) << 28)) : 0u;
       wlut12[v] = wl;

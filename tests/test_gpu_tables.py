@@ -33,7 +33,8 @@ def layout(max_codes: int) -> dict:
     L["wlut12"] = a16(L["clut12"] + 2 * 4096)
     L["wlut12n"] = a16(L["wlut12"] + 16 * 4096)
     L["c15"] = a16(L["wlut12n"] + 8 * 4096)
-    L["lim"] = a16(L["c15"] + 32768)
+    L["len12"] = a16(L["c15"] + 32768)
+    L["lim"] = a16(L["len12"] + 4096)
     L["base"] = L["lim"] + 8 * 33
     L["lj"] = a16(L["base"] + 8 * 33)
     L["ljsym"] = a16(L["lj"] + 4 * max_codes)
@@ -86,10 +87,11 @@ def test_canonical_tables_match_general_builder(env):
         assert np.array_equal(hf[1:7], hg[1:7]), (hf[:7], hg[:7])  # max_len ncodes lut_bits alphabet status complete
         ncodes = int(hf[2])
         assert ncodes == len(book.entries)
-        for name in ("lut", "cnt", "dlut8", "clut8", "wlut8", "lut12", "clut12", "wlut12", "wlut12n", "c15"):
+        for name in ("lut", "cnt", "dlut8", "clut8", "wlut8", "lut12", "clut12", "wlut12", "wlut12n", "c15",
+                     "len12"):
             nxt = {"lut": "cnt", "cnt": "dlut8", "dlut8": "clut8", "clut8": "wlut8", "wlut8": "lut12",
                    "lut12": "clut12", "clut12": "wlut12", "wlut12": "wlut12n", "wlut12n": "c15",
-                   "c15": "lim"}[name]
+                   "c15": "len12", "len12": "lim"}[name]
             assert np.array_equal(f[L[name]:L[nxt]], g[L[name]:L[nxt]]), (name, book.max_len, ncodes)
         for name, w in (("lj", 4), ("ljsym", 2), ("ljlen", 1)):
             assert np.array_equal(f[L[name]:L[name] + w * ncodes], g[L[name]:L[name] + w * ncodes]), name
