@@ -141,61 +141,66 @@ __global__ void __launch_bounds__(DQ_THREADS) k_dq_reduce(const uint16_t* __rest
   }
 }
 
-// pass 2 (one CTA): exclusive segmented scan of the tile aggregates -> tile
-// prefixes, 4096 aggregates at a time: coalesced loads into shared memory,
-// each thread scans 4 consecutive ones, the block scans the thread totals,
-// coalesced stores back (a carry links the chunks)
-constexpr int SCAN_ITEMS = 4;  // 4096 aggregates (36 KB of shared memory) per chunk
-__global__ void __launch_bounds__(1024) k_dq_scan(long long* __restrict__ aggs, const uint8_t* __restrict__ resets,
-                                                  uint64_t ntiles) {
-  __shared__ long long s_v[1024 * SCAN_ITEMS];
-  __shared__ uint8_t s_r[1024 * SCAN_ITEMS];
+// pass 2: exclusive segmented scan of the tile aggregates in two levels --
+// every CTA scans 1024 aggregates (coalesced) and keeps its total, one CTA
+// scans the totals; the apply pass combines the two prefixes
+__device__ __forceinline__ Seg block_excl_seg(Seg v, Seg& total) {
   __shared__ Seg s_w[32];
-  __shared__ Seg s_carry;
-  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) s_carry = Seg{0, 0};
-  for (uint64_t c0 = 0; c0 < ntiles; c0 += 1024 * SCAN_ITEMS) {
-    const uint32_t m = (uint32_t)min((uint64_t)1024 * SCAN_ITEMS, ntiles - c0);
-    for (uint32_t i = tid; i < 1024 * SCAN_ITEMS; i += 1024) {
-      s_v[i] = i < m ? aggs[c0 + i] : 0ll;
-      s_r[i] = i < m ? resets[c0 + i] : (uint8_t)0;
-    }
-    __syncthreads();
-    Seg t{0, 0};
+  const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  Seg x = v;
 #pragma unroll
-    for (int k = 0; k < SCAN_ITEMS; ++k) t = seg_op(t, Seg{s_v[tid * SCAN_ITEMS + k], s_r[tid * SCAN_ITEMS + k]});
-    Seg x = t;
+  for (int o = 1; o < 32; o <<= 1) {
+    Seg y{__shfl_up_sync(0xffffffffu, x.s, o), __shfl_up_sync(0xffffffffu, x.r, o)};
+    if ((int)lane >= o) x = seg_op(y, x);
+  }
+  if (lane == 31) s_w[warp] = x;
+  __syncthreads();
+  if (warp == 0) {
+    Seg z = lane < (blockDim.x >> 5) ? s_w[lane] : Seg{0, 0};
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      Seg y{__shfl_up_sync(0xffffffffu, x.s, o), __shfl_up_sync(0xffffffffu, x.r, o)};
-      if ((int)lane >= o) x = seg_op(y, x);
+      Seg y{__shfl_up_sync(0xffffffffu, z.s, o), __shfl_up_sync(0xffffffffu, z.r, o)};
+      if ((int)lane >= o) z = seg_op(y, z);
     }
-    if (lane == 31) s_w[warp] = x;
-    __syncthreads();
-    if (warp == 0) {
-      Seg z = s_w[lane];
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        Seg y{__shfl_up_sync(0xffffffffu, z.s, o), __shfl_up_sync(0xffffffffu, z.r, o)};
-        if ((int)lane >= o) z = seg_op(y, z);
-      }
-      s_w[lane] = z;
-    }
-    __syncthreads();
-    Seg pre = s_carry;
-    if (warp) pre = seg_op(pre, s_w[warp - 1]);
-    const Seg lp{__shfl_up_sync(0xffffffffu, x.s, 1), __shfl_up_sync(0xffffffffu, x.r, 1)};
-    if (lane) pre = seg_op(pre, lp);
-#pragma unroll
-    for (int k = 0; k < SCAN_ITEMS; ++k) {
-      const Seg a{s_v[tid * SCAN_ITEMS + k], s_r[tid * SCAN_ITEMS + k]};
-      s_v[tid * SCAN_ITEMS + k] = pre.s;  // exclusive prefix: the running value before the tile
-      pre = seg_op(pre, a);
-    }
-    __syncthreads();
-    for (uint32_t i = tid; i < m; i += 1024) aggs[c0 + i] = s_v[i];
-    if (tid == 0) s_carry = seg_op(s_carry, s_w[31]);
-    __syncthreads();
+    s_w[lane] = z;
+  }
+  __syncthreads();
+  total = s_w[(blockDim.x >> 5) - 1];
+  Seg pre{0, 0};
+  if (warp) pre = s_w[warp - 1];
+  const Seg lp{__shfl_up_sync(0xffffffffu, x.s, 1), __shfl_up_sync(0xffffffffu, x.r, 1)};
+  if (lane) pre = seg_op(pre, lp);
+  __syncthreads();
+  return pre;
+}
+
+__global__ void __launch_bounds__(1024) k_dq_scan_local(long long* __restrict__ aggs, uint8_t* __restrict__ resets,
+                                                        uint64_t ntiles, long long* __restrict__ bsum,
+                                                        uint8_t* __restrict__ breset) {
+  const uint64_t i = (uint64_t)blockIdx.x * 1024 + threadIdx.x;
+  const Seg a = i < ntiles ? Seg{aggs[i], resets[i]} : Seg{0, 0};
+  Seg tot;
+  const Seg pre = block_excl_seg(a, tot);
+  if (i < ntiles) {
+    aggs[i] = pre.s;                 // prefix within the block
+    resets[i] = (uint8_t)pre.r;      // a reset before this tile inside the block
+  }
+  if (threadIdx.x == 0) {
+    bsum[blockIdx.x] = tot.s;
+    breset[blockIdx.x] = (uint8_t)tot.r;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_dq_scan_top(long long* __restrict__ bsum, uint8_t* __restrict__ breset,
+                                                      uint64_t nb) {
+  Seg carry{0, 0};
+  for (uint64_t b0 = 0; b0 < nb; b0 += 1024) {
+    const uint64_t i = b0 + threadIdx.x;
+    const Seg a = i < nb ? Seg{bsum[i], breset[i]} : Seg{0, 0};
+    Seg tot;
+    const Seg pre = seg_op(carry, block_excl_seg(a, tot));
+    if (i < nb) bsum[i] = pre.s;     // exclusive prefix of the block totals
+    carry = seg_op(carry, tot);
   }
 }
 
@@ -236,12 +241,15 @@ __global__ void __launch_bounds__(DQ_THREADS) k_dequant(const uint16_t* __restri
                                                         const long long* __restrict__ ounits, uint64_t nout,
                                                         double twice_eb, int32_t mid,
                                                         const long long* __restrict__ prefix,
+                                                        const uint8_t* __restrict__ resets_pre,
+                                                        const long long* __restrict__ bpre,
                                                         double* __restrict__ out, DqWork* w) {
   __shared__ Seg s_warp[DQ_THREADS / 32];
   DqTile T;
   dq_tile(codes, n, oidx, ounits, nout, mid, blockIdx.x, nullptr, T, s_warp);
   const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  Seg pre{prefix[blockIdx.x], 0};
+  // tile prefix: the block prefix unless a reset precedes the tile in its block
+  Seg pre{resets_pre[blockIdx.x] ? prefix[blockIdx.x] : bpre[blockIdx.x >> 10] + prefix[blockIdx.x], 0};
   if (warp) pre = seg_op(pre, s_warp[warp - 1]);
   const Seg lp{__shfl_up_sync(0xffffffffu, T.x.s, 1), __shfl_up_sync(0xffffffffu, T.x.r, 1)};
   if (lane) pre = seg_op(pre, lp);
@@ -305,7 +313,8 @@ using namespace bh;
 static uint64_t dq_tiles(uint64_t n) { return (n + DQ_TILE - 1) / DQ_TILE; }
 
 extern "C" size_t bh_dequant_workspace_bytes(uint64_t n) {
-  return align16(sizeof(DqWork)) + align16(8 * (dq_tiles(n) + 1)) + align16(dq_tiles(n) + 1);
+  const uint64_t nt = dq_tiles(n), nb = (nt + 1023) / 1024 + 1;
+  return align16(sizeof(DqWork)) + align16(8 * (nt + 1)) + align16(nt + 1) + align16(8 * nb) + align16(nb);
 }
 
 // twice_eb = 2^e with -149 <= e <= 104 (f32 keeps every multiple below 2^24)
@@ -344,9 +353,14 @@ extern "C" int bh_dequantize(const uint16_t* codes_dev, uint64_t n, const int64_
                                                          (int32_t)midpoint, aggs, resets, w);
       else
         k_dq_reduce_plain<<<(unsigned)nt, DQ_THREADS, 0, st>>>(codes_dev, n, (int32_t)midpoint, aggs, resets);
-      k_dq_scan<<<1, 1024, 0, st>>>(aggs, resets, nt);
+      const uint64_t nb = (nt + 1023) / 1024;
+      long long* bsum = reinterpret_cast<long long*>(resets + align16(nt + 1));
+      uint8_t* breset = reinterpret_cast<uint8_t*>(bsum) + align16(8 * (nb + 1));
+      k_dq_scan_local<<<(unsigned)nb, 1024, 0, st>>>(aggs, resets, nt, bsum, breset);
+      k_dq_scan_top<<<1, 1024, 0, st>>>(bsum, breset, nb);
       k_dequant<<<(unsigned)nt, DQ_THREADS, DQ_THREADS * (DQ_ITEMS + 1) * sizeof(double), st>>>(
-          codes_dev, n, outlier_idx_dev, un, n_outliers, twice_eb, (int32_t)midpoint, aggs, out_dev, w);
+          codes_dev, n, outlier_idx_dev, un, n_outliers, twice_eb, (int32_t)midpoint, aggs, resets, bsum, out_dev,
+          w);
     }
     if (cudaMemcpyAsync(inexact_dev, &w->inexact, 4, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
       return BH_CUDA_ERROR;
