@@ -306,9 +306,19 @@ __device__ __forceinline__ uint32_t fone(uint32_t win, const FTab& T) {
 
 // length of one codeword from the 12-bit count table (second start, or the end
 // of the only whole codeword); codes longer than 12 bits take the limit search
+// (wide modes: len12; the narrow mode keeps no len12 and reads the count table)
+template <int MODE>
 __device__ __forceinline__ uint32_t clen(uint32_t win, const FTab& T) {
-  const uint32_t l = lds8(T.len12 + (win >> (32 - FB)));
-  if (l) return l;
+  if (MODE == M_NARROW) {
+    const uint32_t y = lds16(T.c12 + ((win >> (32 - FB)) << 1));
+    if (y) {
+      const uint32_t m = y & 0xffeu;
+      return m ? __ffs(m) - 1 : (y >> 12);
+    }
+  } else {
+    const uint32_t l = lds8(T.len12 + (win >> (32 - FB)));
+    if (l) return l;
+  }
   return (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
 }
 
@@ -556,6 +566,7 @@ __device__ bool fdecode_global(SR& r, uint32_t c, uint16_t* out, uint64_t at, ui
 // longer than 12 bits.
 // Per-codeword lock-step walk: cheaper than the mask walk when a 12-bit entry
 // holds only a couple of codewords (long-code books, wide layout).
+template <int MODE>
 __device__ __forceinline__ bool resync_step(uint32_t base_s, uint32_t eo, uint32_t co, uint32_t xo, uint32_t en,
                                             uint32_t stop, const FTab& T, uint32_t& cn, uint32_t& xn) {
   uint32_t po = eo, pn = en, no = 0, nn = 0;
@@ -566,13 +577,13 @@ __device__ __forceinline__ bool resync_step(uint32_t base_s, uint32_t eo, uint32
     if (pn >= stop) { cn = nn; xn = pn; return true; }
     if (po == pn) { cn = nn + (co - no); xn = xo; return true; }
     if (po < pn) {
-      const uint32_t l = clen(ro.peek(), T);
+      const uint32_t l = clen<MODE>(ro.peek(), T);
       if (!l) return false;
       ro.skip(l);
       po += l;
       ++no;
     } else {
-      const uint32_t l = clen(rn.peek(), T);
+      const uint32_t l = clen<MODE>(rn.peek(), T);
       if (!l) return false;
       rn.skip(l);
       pn += l;
@@ -586,7 +597,7 @@ __device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co
                                        uint32_t stop, const FTab& T, uint32_t& cn, uint32_t& xn) {
   // long-code books (wide layouts): a 12-bit entry holds a codeword or two, so
   // the plain per-codeword walk is cheaper there
-  if (MODE != M_NARROW) return resync_step(base_s, eo, co, xo, en, stop, T, cn, xn);
+  if (MODE != M_NARROW) return resync_step<MODE>(base_s, eo, co, xo, en, stop, T, cn, xn);
   uint32_t po = eo, pn = en, no = 0, nn = 0;
   SR ro, rn;
   ro.init(base_s, po);
@@ -827,6 +838,70 @@ __device__ __forceinline__ void flush_aligned(uint16_t* __restrict__ out, uint64
   }
 }
 
+// The seam candidates of a tile's first slot (inter_sync, sync_decoder.py:
+// 116-149): for every seed offset o < max_len, the codewords the slot holds
+// when entered at b0 + o, and its exit.  Instead of one lock-step walk per
+// candidate, the warp reads the length of the codeword at each of the first
+// 64 bit offsets once (lane p: offsets p and 32 + p), marks the starts of the
+// parse from b0 in a 64-bit mask, and then every candidate follows its own
+// parse with shuffles of those lengths until it lands on a start of the b0
+// parse (from there both parses coincide: count = own codewords so far +
+// the b0 parse's codewords from that start), reaches the slot end, or leaves
+// the 64-bit window (then the lock-step walk finishes it).
+template <int MODE>
+__device__ __forceinline__ void cand_chase(uint32_t base_s, uint32_t b0, uint32_t c0, uint32_t x0, uint32_t stop0,
+                                           const FTab& T, uint32_t& cand_c, uint32_t& cand_x) {
+  const uint32_t lane = threadIdx.x & 31;
+  const uint32_t span = stop0 > b0 ? stop0 - b0 : 0u;
+  const uint32_t p0 = b0 + lane, j = p0 >> 5, off = p0 & 31;
+  const uint32_t w0 = lds32(skew_addr(base_s, j)), w1 = lds32(skew_addr(base_s, j + 1));
+  const uint32_t w2 = lds32(skew_addr(base_s, j + 2));
+  const uint32_t La = clen<MODE>(__funnelshift_l(w1, w0, off), T);  // codeword length at offset lane
+  const uint32_t Lb = clen<MODE>(__funnelshift_l(w2, w1, off), T);  // ... at offset 32 + lane
+  // starts of the parse from b0 inside [0, min(span, 64))
+  const uint32_t lim = min(span, 64u);
+  unsigned long long M = 0;
+  for (uint32_t p = 0; p < lim;) {
+    M |= 1ull << p;
+    const uint32_t a = __shfl_sync(0xffffffffu, La, p & 31), bb = __shfl_sync(0xffffffffu, Lb, p & 31);
+    const uint32_t l = p < 32 ? a : bb;
+    if (!l) break;
+    p += l;
+  }
+  // every candidate lane follows its own parse
+  const bool cand = lane < T.max_len;
+  uint32_t q = lane, k = 0, how = cand ? 0u : 4u;  // 0 running, 1 met, 2 slot end, 3 left the window, 4 invalid / none
+  while (__any_sync(0xffffffffu, how == 0)) {
+    const uint32_t a = __shfl_sync(0xffffffffu, La, q & 31), bb = __shfl_sync(0xffffffffu, Lb, q & 31);
+    if (how == 0) {
+      if (q >= span) {
+        how = 2;
+      } else if (q >= 64) {
+        how = 3;
+      } else if ((M >> q) & 1ull) {
+        how = 1;
+      } else {
+        const uint32_t l = q < 32 ? a : bb;
+        if (!l) how = 4; else { q += l; ++k; }
+      }
+    }
+  }
+  if (!cand) return;
+  if (how == 1) {
+    cand_c = k + c0 - (uint32_t)__popcll(M & ((1ull << q) - 1ull));
+    cand_x = x0;
+  } else if (how == 2) {
+    cand_c = k;
+    cand_x = b0 + q;
+  } else if (how == 3) {
+    uint32_t cn, xn;
+    if (resync<MODE>(base_s, b0, c0, x0, b0 + q, stop0, T, cn, xn)) { cand_c = k + cn; cand_x = xn; }
+    else cand_x = 0xffffffffu;
+  } else {
+    cand_x = 0xffffffffu;  // no codeword matches from this seed
+  }
+}
+
 // Entries and counts of one tile (lane = subsequence); positions are relative
 // to the tile buffer's first bit `wb0`.  GAP: boundary + gap byte; SYNC:
 // intra-sequence chain rounds plus the seam seed from the predecessor tile's
@@ -917,9 +992,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
       // the true seed lies within the codeword straddling the boundary, so
       // only offsets below the longest code length are candidates
 #ifndef BH_X_NOCAND
-      if (lane < T.max_len) {
-        if (!resync<MODE>(base_s, b0, c0, x0, b0 + lane, stop0, T, cand_c, cand_x)) cand_x = 0xffffffffu;
-      }
+      cand_chase<MODE>(base_s, b0, c0, x0, stop0, T, cand_c, cand_x);
 #endif
       indep = __all_sync(0xffffffffu, cand_x == x0);
     }
