@@ -183,6 +183,9 @@ int bh_workspace_reset(void *workspace_dev, size_t workspace_bytes, void *cuda_s
  * not put whole sequences in a tile. */
 int bh_tuner_class_freq(const bh_stream *s, const bh_tune *tune, const void *workspace_dev,
                         uint64_t *freq_host, uint32_t n, void *cuda_stream);
+/* 1 when the fused single-kernel decoder takes this stream and variant (the
+ * only path for chunks: first_entry or BH_STREAM_COUNT_IS_CAPACITY), else 0. */
+int bh_fused_supported(const bh_stream *s, int variant);
 /* Synchronous convenience: decode, finish any extra seam passes, read report. */
 int bh_decode(const bh_stream *s, int variant, const bh_tune *tune, uint16_t *out_dev,
               void *workspace_dev, size_t workspace_bytes, bh_report *report_host,

@@ -101,6 +101,7 @@ SIGNATURES = {
     "bh_symbol_histogram": (I32, [P, U64, U32, P, P]),
     "bh_build_lengths": (I32, [P, U32, P, P, P]),
     "bh_tuner_class_freq": (I32, [P, P, P, P, U32, P]),
+    "bh_fused_supported": (I32, [P, I32]),
     "bh_dequant_workspace_bytes": (SZ, [U64]),
     "bh_dequantize": (I32, [P, U64, P, P, P, U64, C.c_double, U32, I32, P, P, SZ, P, P]),
 }

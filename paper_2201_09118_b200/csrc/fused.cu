@@ -842,29 +842,47 @@ __device__ __forceinline__ void flush_aligned(uint16_t* __restrict__ out, uint64
 // 116-149): for every seed offset o < max_len, the codewords the slot holds
 // when entered at b0 + o, and its exit.  Instead of one lock-step walk per
 // candidate, the warp reads the length of the codeword at each of the first
-// 64 bit offsets once (lane p: offsets p and 32 + p), marks the starts of the
-// parse from b0 in a 64-bit mask, and then every candidate follows its own
+// 32 NG bit offsets once (lane p: offsets p, 32 + p, ...), marks the starts of the
+// parse from b0 in a bit mask, and then every candidate follows its own
 // parse with shuffles of those lengths until it lands on a start of the b0
 // parse (from there both parses coincide: count = own codewords so far +
 // the b0 parse's codewords from that start), reaches the slot end, or leaves
-// the 64-bit window (then the lock-step walk finishes it).
+// the window (then the lock-step walk finishes it).
+#ifndef BH_CHASE_G
+#define BH_CHASE_G 3  // 32-bit groups of offsets the chase covers (96 bits)
+#endif
 template <int MODE>
 __device__ __forceinline__ void cand_chase(uint32_t base_s, uint32_t b0, uint32_t c0, uint32_t x0, uint32_t stop0,
                                            const FTab& T, uint32_t& cand_c, uint32_t& cand_x) {
+  constexpr uint32_t NG = BH_CHASE_G, WIN = 32 * NG;
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t span = stop0 > b0 ? stop0 - b0 : 0u;
   const uint32_t p0 = b0 + lane, j = p0 >> 5, off = p0 & 31;
-  const uint32_t w0 = lds32(skew_addr(base_s, j)), w1 = lds32(skew_addr(base_s, j + 1));
-  const uint32_t w2 = lds32(skew_addr(base_s, j + 2));
-  const uint32_t La = clen<MODE>(__funnelshift_l(w1, w0, off), T);  // codeword length at offset lane
-  const uint32_t Lb = clen<MODE>(__funnelshift_l(w2, w1, off), T);  // ... at offset 32 + lane
-  // starts of the parse from b0 inside [0, min(span, 64))
-  const uint32_t lim = min(span, 64u);
-  unsigned long long M = 0;
+  uint32_t L[NG];  // L[g]: length of the codeword at offset 32 g + lane
+  {
+    uint32_t wa = lds32(skew_addr(base_s, j));
+#pragma unroll
+    for (uint32_t g = 0; g < NG; ++g) {
+      const uint32_t wb = lds32(skew_addr(base_s, j + 1 + g));
+      L[g] = clen<MODE>(__funnelshift_l(wb, wa, off), T);
+      wa = wb;
+    }
+  }
+  auto len_at = [&](uint32_t p) -> uint32_t {  // every lane calls it (shuffles)
+    uint32_t v = 0;
+#pragma unroll
+    for (uint32_t g = 0; g < NG; ++g) {
+      const uint32_t x = __shfl_sync(0xffffffffu, L[g], p & 31);
+      v = (p >> 5) == g ? x : v;
+    }
+    return v;
+  };
+  // starts of the parse from b0 inside [0, min(span, WIN))
+  const uint32_t lim = min(span, WIN);
+  unsigned long long M0 = 0, M1 = 0;
   for (uint32_t p = 0; p < lim;) {
-    M |= 1ull << p;
-    const uint32_t a = __shfl_sync(0xffffffffu, La, p & 31), bb = __shfl_sync(0xffffffffu, Lb, p & 31);
-    const uint32_t l = p < 32 ? a : bb;
+    if (p < 64) M0 |= 1ull << p; else M1 |= 1ull << (p - 64);
+    const uint32_t l = len_at(p);
     if (!l) break;
     p += l;
   }
@@ -872,23 +890,21 @@ __device__ __forceinline__ void cand_chase(uint32_t base_s, uint32_t b0, uint32_
   const bool cand = lane < T.max_len;
   uint32_t q = lane, k = 0, how = cand ? 0u : 4u;  // 0 running, 1 met, 2 slot end, 3 left the window, 4 invalid / none
   while (__any_sync(0xffffffffu, how == 0)) {
-    const uint32_t a = __shfl_sync(0xffffffffu, La, q & 31), bb = __shfl_sync(0xffffffffu, Lb, q & 31);
+    const uint32_t l = len_at(q);
     if (how == 0) {
-      if (q >= span) {
-        how = 2;
-      } else if (q >= 64) {
-        how = 3;
-      } else if ((M >> q) & 1ull) {
-        how = 1;
-      } else {
-        const uint32_t l = q < 32 ? a : bb;
-        if (!l) how = 4; else { q += l; ++k; }
-      }
+      const bool inM = q < 64 ? ((M0 >> q) & 1ull) : q < WIN ? ((M1 >> (q - 64)) & 1ull) : false;
+      if (q >= span) how = 2;
+      else if (q >= WIN) how = 3;
+      else if (inM) how = 1;
+      else if (!l) how = 4;
+      else { q += l; ++k; }
     }
   }
   if (!cand) return;
   if (how == 1) {
-    cand_c = k + c0 - (uint32_t)__popcll(M & ((1ull << q) - 1ull));
+    const uint32_t before = q < 64 ? (uint32_t)__popcll(M0 & ((1ull << q) - 1ull))
+                                   : (uint32_t)__popcll(M0) + (uint32_t)__popcll(M1 & ((1ull << (q - 64)) - 1ull));
+    cand_c = k + c0 - before;
     cand_x = x0;
   } else if (how == 2) {
     cand_c = k;
@@ -992,7 +1008,13 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
       // the true seed lies within the codeword straddling the boundary, so
       // only offsets below the longest code length are candidates
 #ifndef BH_X_NOCAND
-      cand_chase<MODE>(base_s, b0, c0, x0, stop0, T, cand_c, cand_x);
+      if (MODE != M_NARROW) {
+        cand_chase<MODE>(base_s, b0, c0, x0, stop0, T, cand_c, cand_x);
+      } else if (lane < T.max_len) {
+        // short codes: the entry-at-a-time mask walk is cheaper than a chase
+        // over 64 offsets (up to 64 codewords)
+        if (!resync<MODE>(base_s, b0, c0, x0, b0 + lane, stop0, T, cand_c, cand_x)) cand_x = 0xffffffffu;
+      }
 #endif
       indep = __all_sync(0xffffffffu, cand_x == x0);
     }

@@ -234,6 +234,9 @@ def decode_shard(streams, rank: int = 0, world: int = 1, variant: str = "gap", d
         # (same symbols -- the synchronised state is the unique fixpoint)
         sync_ok = variant != "gap" and kraft_complete(book)
         var = _lib.VARIANT_SYNC if sync_ok else _lib.VARIANT_GAP
+        if not lib.bh_fused_supported(C.byref(c), var):
+            raise ValueError("sharded decode needs the fused decoder, which does not take this layout "
+                             "(sequences of more than 16384 bits per tile, or forced knobs)")
         tune = make_tune(max_len=book.max_len, min_len=book.min_len)
         if len(plan) > 1:
             tune.ctas = max(1, round(sms * tb / max(total_bits, 1)))

@@ -72,7 +72,10 @@ def main():
             "gap_tuned": ph.gap_decoder.decode(st, tuner_config=ph.TunerConfig(t_high=th)),
             "sync_tuned": ph.sync_decoder.decode(st, tuner_config=ph.TunerConfig(t_high=th)),
         }
-        if (lay[0] * lay[1] * lay[2]) % 128 == 0 and st.num_seqs > 2 and rng.random() < 0.5:
+        from paper_2201_09118_b200 import _lib as _l
+        from paper_2201_09118_b200.device import device_stream
+        shardable = bool(_l.load().bh_fused_supported(device_stream(st).ref, _l.VARIANT_GAP))
+        if shardable and (lay[0] * lay[1] * lay[2]) % 128 == 0 and st.num_seqs > 2 and rng.random() < 0.5:
             from paper_2201_09118_b200 import shard
             world = int(rng.integers(2, 5))
             v = "gap" if rng.random() < 0.5 else "sync"
