@@ -1196,7 +1196,6 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   // the seam fix-up reads in-range predecessors from shared memory
   constexpr uint32_t SX = VAR == BH_VARIANT_SYNC ? MAX_SMEM_TILES : 1;
   __shared__ unsigned long long s_texit[SX];
-  __shared__ uint8_t s_tff[SX];
   const uint32_t ep = *(volatile const unsigned int*)a.ws_hdr + 1u;
   const TableHdr* hdr = static_cast<const TableHdr*>(a.table);
   if (VAR == BH_VARIANT_SYNC && !hdr->complete) {
@@ -1272,7 +1271,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   T.kind = hdr->kind;
   T.max_len = hdr->max_len ? min(hdr->max_len, 32u) : 32u;
   if (VAR == BH_VARIANT_SYNC)
-    for (uint32_t i = threadIdx.x; i < SX; i += blockDim.x) { s_texit[i] = 0; s_tff[i] = 0; }
+    for (uint32_t i = threadIdx.x; i < SX; i += blockDim.x) s_texit[i] = 0;
   for (uint32_t i = threadIdx.x; i < TUNE_CLASSES; i += blockDim.x) s_cls[i] = 0;
   if (threadIdx.x == 0) {
     s_next = W;  // phase 2 starts with tile t0 + warp index
@@ -1326,10 +1325,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       else a.cand[tile * 32 + lane] = (uint16_t)min(cand, 0xffffu);
       if (lane == 0) {
         a.tile_dlt[tile] = fullfix ? FULL_FIX : 0;
-        if (srange) {
-          s_tff[tile - t0] = fullfix ? 1 : 0;
-          *(volatile unsigned long long*)&s_texit[tile - t0] = dsc;
-        }
+        if (srange) *(volatile unsigned long long*)&s_texit[tile - t0] = dsc;
       }
     }
     ++kidx;
@@ -1373,7 +1369,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         unsigned long long dp;
         const unsigned long long ds = sm_own ? *(volatile unsigned long long*)&s_texit[tk - t0]
                                              : ld_relaxed(a.exit_desc + tk);
-        const bool ff = sm_own ? s_tff[tk - t0] != 0 : a.tile_dlt[tk] == FULL_FIX;
+        const bool ff = a.tile_dlt[tk] == FULL_FIX;  // written by this warp's lane 0 in the count loop
         if (sm_pred) {
           while (!desc_ready(dp = *(volatile unsigned long long*)&s_texit[tk - 1 - t0], ep)) __nanosleep(32);
         } else {
@@ -1419,8 +1415,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         const uint32_t o = (uint32_t)((dp & D_VAL) - st * a.seq_bits);
         const unsigned long long ds = sm_own ? *(volatile unsigned long long*)&s_texit[st - t0]
                                              : ld_relaxed(a.exit_desc + st);
-        const bool ff = sm_own ? s_tff[st - t0] != 0
-                               : __shfl_sync(0xffffffffu, lane == 0 ? (uint32_t)(a.tile_dlt[st] == FULL_FIX) : 0u, 0) != 0;
+        const bool ff = __shfl_sync(0xffffffffu, lane == 0 ? (uint32_t)(a.tile_dlt[st] == FULL_FIX) : 0u, 0) != 0;
         if ((ds & D_INC) && !ff) {  // first-slot swap behind a dependent predecessor
           if (o >= 32) {
             bad = true;

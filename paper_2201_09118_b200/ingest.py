@@ -120,7 +120,10 @@ class _Stager:
         self.k = 0
 
     def file_to_device(self, f, file_off: int, nbytes: int, dst_u8):
-        """Copy file bytes [file_off, +nbytes) into the device byte tensor dst_u8."""
+        """Copy file bytes [file_off, +nbytes) into the device byte tensor dst_u8.
+        The copies wait for the work already queued on the caller's stream
+        (dst_u8 was allocated -- and zero-filled -- there)."""
+        self.copy.wait_stream(self.torch.cuda.current_stream(dst_u8.device))
         f.seek(file_off)
         pos = 0
         while pos < nbytes:
