@@ -106,6 +106,7 @@ struct FusedArgs {
   uint32_t first_entry;  // bh_stream.first_entry
   uint32_t count_cap;    // BH_STREAM_COUNT_IS_CAPACITY: nsym is the output capacity, the count is reported
   uint32_t spl;          // stream subsequences per lane ("virtual" subsequence = spl real ones)
+  uint32_t sbr;          // stream subsequence bits (sb / spl)
   uint64_t nsub_r;       // real subsequences (gap array length)
   uint32_t wide;         // table layout: 1 = wlut12, 0 = replicated wlut8 (+ lut12 if has_l12)
   uint32_t t_lim, t_c12, t_wp, t_l12;  // shared-memory table offsets (bytes)
@@ -670,10 +671,6 @@ __device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co
   }
 }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
 __device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
@@ -706,24 +703,56 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
 __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
-// stage the words of `tile` (16 B chunks, one per lane per step)
-// Stage a tile's words: 16-byte cp.async chunks into the warp's landing
-// buffer (few, wide L2 requests); skew_in() then spreads them into the skewed
-// decode buffer.  Returns the bit offset of logical word 0.
-__device__ __forceinline__ uint64_t stage_words(const FusedArgs& a, uint64_t tile, uint32_t* land, uint32_t& nch) {
-  const uint32_t lane = threadIdx.x & 31;
+// Per-warp word staging: one bulk (TMA) copy of a tile's words into the
+// warp's landing buffer, completing on the warp's own mbarrier; skew_in()
+// then spreads them into the skewed decode buffer.  At most one copy is in
+// flight per warp (wstage_wait consumes it).
+struct WStage {
+  uint32_t bar;    // shared address of the warp's mbarrier
+  uint32_t phase;  // parity of the next completion
+  bool pending;
+};
+
+__device__ __forceinline__ void wstage_init(WStage& ws, uint32_t bar) {
+  ws.bar = bar;
+  ws.phase = 0;
+  ws.pending = false;
+  if ((threadIdx.x & 31) == 0) {
+    mbar_init(bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+}
+
+// Stage the words of `tile`; returns the bit offset of logical word 0.  The
+// caller has synced the warp after its last read of the landing buffer.
+__device__ __forceinline__ uint64_t stage_words(const FusedArgs& a, uint64_t tile, uint32_t land_s, uint32_t& nch,
+                                                WStage& ws) {
   const uint64_t s0 = tile * (uint64_t)a.seq_bits;
   const uint64_t w0 = (s0 >> 5) & ~3ull;
   uint64_t w1 = ((s0 + a.seq_bits) >> 5) + HALO_WORDS;
   w1 = (w1 + 3) & ~3ull;
   if (w1 > a.words_alloc) w1 = a.words_alloc;
   nch = (uint32_t)((w1 - w0) >> 2);
-  for (uint32_t c = lane; c < nch; c += 32) cp_async16(land + 4 * c, a.words + w0 + 4 * c);
+  if ((threadIdx.x & 31) == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier reads of the buffer -> async proxy
+    if (nch) {
+      mbar_expect_tx(ws.bar, 16 * nch);
+      bulk_g2s(land_s, a.words + w0, 16 * nch, ws.bar);
+    } else {
+      mbar_arrive(ws.bar);
+    }
+  }
+  ws.pending = true;
   return w0 * 32;
+}
+
+__device__ __forceinline__ void wstage_wait(WStage& ws) {
+  if (!ws.pending) return;
+  mbar_wait(ws.bar, ws.phase);
+  ws.phase ^= 1u;
+  ws.pending = false;
 }
 
 // landing buffer (contiguous) -> decode buffer (skew_addr layout); the caller
@@ -962,7 +991,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
       // hold exactly the same codewords); a corrupt inner entry sends the
       // decode to the reference-structured pipeline, which reproduces the
       // reference's error
-      const uint32_t sbr = sb / a.spl;
+      const uint32_t sbr = a.sbr;
       for (uint32_t k = 1; k < a.spl; ++k) {
         const uint64_t jr = j * a.spl + k;
         if (jr >= a.nsub_r) break;
@@ -1191,6 +1220,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   __shared__ uint32_t s_next;  // phase 2: next tile of the range to take
   __shared__ unsigned long long s_tcount, s_tseam;  // phase clocks (count loop end, seam fix-up end)
   __shared__ uint32_t s_cls[TUNE_CLASSES];           // tuner: sequences per class
+  __shared__ __align__(8) unsigned long long s_wbar[FUSED_MAX_WARPS];  // per-warp word-staging mbarriers
   __shared__ uint32_t s_tcnt[MAX_SMEM_TILES];  // symbols per tile of the range (short ranges)
   // SYNC, short ranges: the range's exit descriptors and full-fix flags, so
   // the seam fix-up reads in-range predecessors from shared memory
@@ -1205,7 +1235,6 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   }
   const uint32_t lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   unsigned char* pw = sm + a.tables_bytes + (size_t)wib * a.per_warp_bytes;
-  uint32_t* const wbase = reinterpret_cast<uint32_t*>(pw);
   const uint32_t wbase_s = smem_u32(pw);
   const uint32_t stg_s = wbase_s + 8 * a.wpb;  // two word buffers, then staging
   const uint16_t* stg = reinterpret_cast<const uint16_t*>(pw + 8 * (size_t)a.wpb);
@@ -1249,13 +1278,13 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   }
   // per warp: a landing buffer for the cp.async chunks of the next tile and
   // the skewed decode buffer of the current one
-  uint32_t* const land = wbase;
   const uint32_t land_s = wbase_s, dbuf_s = wbase_s + 4 * a.wpb;
   uint64_t tile = t0 + wib;
   uint64_t wb_a = 0, wb_b = 0;
   uint32_t nch_a = 0, nch_b = 0;
-  if (tile < t1) wb_a = stage_words(a, tile, land, nch_a);
-  cp_commit();
+  WStage wst;
+  wstage_init(wst, smem_u32(&s_wbar[wib]));
+  if (tile < t1) wb_a = stage_words(a, tile, land_s, nch_a, wst);
   FTab T;
   T.wl = MODE != M_NARROW ? sm_s : sm_s + 16 * (lane & 7);
   T.dsh = MODE != M_NARROW ? 32 - FB : 24;
@@ -1301,16 +1330,14 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   if (VAR == BH_VARIANT_GAP && tile < t1) gap_load(tile, gcur);
   for (; tile < t1; tile += W) {
     const uint64_t tn = tile + W;
-    cp_wait<0>();  // this tile's words have landed
-    __syncwarp();
+    wstage_wait(wst);  // this tile's words have landed
     skew_in(land_s, dbuf_s, nch_a);
     __syncwarp();
     if (kidx < 8) MARK(10 + 2 * kidx);
     if (tn < t1) {  // the next tile's words land while this one is counted
-      wb_b = stage_words(a, tn, land, nch_b);
+      wb_b = stage_words(a, tn, land_s, nch_b, wst);
       if (VAR == BH_VARIANT_GAP) gap_load(tn, gnext);
     }
-    cp_commit();
     const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
     uint32_t e, c, cand = 0;
     bool fullfix = false;
@@ -1345,7 +1372,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     wb_a = wb_b;
     nch_a = nch_b;
   }
-  cp_wait<0>();
+  wstage_wait(wst);
   __syncwarp();  // candidate slots written by other lanes are read below
   if (lane == 0) atomicMax(&s_tcount, global_ns());
   MARK(9);
@@ -1433,10 +1460,8 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         }
         // dependent tile: stage its words again and synchronise from the seed
         uint32_t nchs;
-        const uint64_t wbs = stage_words(a, st, land, nchs);
-        cp_commit();
-        cp_wait<0>();
-        __syncwarp();
+        const uint64_t wbs = stage_words(a, st, land_s, nchs, wst);
+        wstage_wait(wst);
         skew_in(land_s, dbuf_s, nchs);
         __syncwarp();
         const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - st * a.sps);
@@ -1553,8 +1578,8 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   // tiles are taken dynamically (a shared counter): a warp that finishes
   // early takes the next tile, so the range's last round is balanced
   tile = t0 + wib;
-  if (tile < t1) wb_a = stage_words(a, tile, land, nch_a);
-  cp_commit();
+  __syncwarp();
+  if (tile < t1) wb_a = stage_words(a, tile, land_s, nch_a, wst);
   bool have_off = false, bulk_pending = false;
   unsigned long long Pc = 0;
   auto grab = [&]() -> uint64_t {
@@ -1591,13 +1616,11 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       C = a.tile_cnt[tile];
       toff = a.tile_off[tile];
     }
-    cp_wait<0>();  // this tile's words have landed
-    __syncwarp();
+    wstage_wait(wst);  // this tile's words have landed
     if (dk < 8) MARK(30 + 3 * dk);
     skew_in(land_s, dbuf_s, nch_a);
     __syncwarp();
-    if (tn < t1) wb_b = stage_words(a, tn, land, nch_b);  // lands while this tile decodes
-    cp_commit();
+    if (tn < t1) wb_b = stage_words(a, tn, land_s, nch_b, wst);  // lands while this tile decodes
     const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
     const uint32_t base_s = dbuf_s;
     const uint32_t b = (uint32_t)((tile * a.sps + lane) * a.sb - wb_a);
@@ -1707,7 +1730,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     nch_a = nch_b;
     tile = tn;
   }
-  cp_wait<0>();
+  wstage_wait(wst);
   if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // staging read (writes land by kernel end)
   if (!have_off) mbar_wait(bar_off, 0);  // keep warp 0's arrival inside the CTA's lifetime
   if (__any_sync(0xffffffffu, bad) && lane == 0) tag_status(a.rep, ep, BH_INVALID);
@@ -1923,6 +1946,7 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.sb = vsb_of(s);
   a.sps = TILE_SUBSEQ;
   a.spl = spl_of(s);
+  a.sbr = s->subseq_bits;
   a.seq_bits = vsb_of(s) * TILE_SUBSEQ;
   a.tb = s->total_bits;
   a.nsym = s->symbol_count;
