@@ -107,7 +107,6 @@ struct FusedArgs {
   uint32_t count_cap;    // BH_STREAM_COUNT_IS_CAPACITY: nsym is the output capacity, the count is reported
   uint32_t spl;          // stream subsequences per lane ("virtual" subsequence = spl real ones)
   uint32_t sbr;          // stream subsequence bits (sb / spl)
-  uint16_t* half;        // GAP, spl 2, M_WIDE3: codewords in each lane's first subsequence (dual-chain decode)
   uint64_t nsub_r;       // real subsequences (gap array length)
   uint32_t wide;         // table layout: 1 = wlut12, 0 = replicated wlut8 (+ lut12 if has_l12)
   uint32_t t_lim, t_c12, t_wp, t_l12;  // shared-memory table offsets (bytes)
@@ -484,54 +483,6 @@ __device__ __forceinline__ bool fdecode3(SR& r, uint32_t c, uint32_t dst, const 
     }
   }
   return true;
-}
-
-// One step of the three-codeword decode: two table entries from one 32-bit
-// window (>= 16 staging bytes must remain).  False: the first entry is a code
-// longer than 12 bits (nothing consumed).
-__device__ __forceinline__ bool dec3_step2(SR& r, uint32_t& dst, int32_t& k2, uint32_t wl) {
-  const uint32_t win = r.peek();
-  const uint2 e = lds64(wl + ((win >> (32 - FB)) << 3));
-  if (!e.y) return false;
-  const uint32_t b1 = (e.y >> 24) & 15u;
-  const uint2 f = lds64(wl + (((win << b1) >> (32 - FB)) << 3));
-  uint32_t odd = dst & 2u, a4 = dst + odd;
-  sts16(dst, e.x);
-  sts32(a4, __funnelshift_r(e.x, e.y, odd << 3));
-  sts32(a4 + 4, e.y);
-  const uint32_t nb1 = e.y >> 28;
-  dst += nb1;
-  uint32_t adv = b1, nb = nb1;
-  if (f.y) {
-    odd = dst & 2u;
-    a4 = dst + odd;
-    sts16(dst, f.x);
-    sts32(a4, __funnelshift_r(f.x, f.y, odd << 3));
-    sts32(a4 + 4, f.y);
-    const uint32_t nb2 = f.y >> 28;
-    dst += nb2;
-    nb += nb2;
-    adv += (f.y >> 24) & 15u;
-  }
-  k2 -= (int32_t)nb;
-  r.skip(adv);
-  return true;
-}
-
-// A lane window of two subsequences decoded as two independent chains (the
-// second entered at its gap byte, with its count from the count phase),
-// interleaved step by step: two dependent table walks per warp instead of one,
-// so each warp hides more of its own shared-memory latency.
-__device__ __forceinline__ bool fdecode3_dual(SR& ra, uint32_t ca, uint32_t da, SR& rb, uint32_t cb, uint32_t db,
-                                              const FTab& T) {
-  const uint32_t wl = pin(T.wl);
-  int32_t ka = 2 * (int32_t)ca, kb = 2 * (int32_t)cb;
-  while (ka >= 16 && kb >= 16) {
-    const bool oka = dec3_step2(ra, da, ka, wl);
-    const bool okb = dec3_step2(rb, db, kb, wl);
-    if (!oka || !okb) break;  // a long code: each chain finishes on its own
-  }
-  return fdecode3(ra, (uint32_t)(ka >> 1), da, T) & fdecode3(rb, (uint32_t)(kb >> 1), db, T);
 }
 
 template <int MODE>
@@ -1048,7 +999,6 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
         if (ek < x || ek > stop) { resync_needed = true; break; }
         if (!fcount(r, x, ek, T, c)) bad = true;
         if (x != ek) { resync_needed = true; break; }
-        if (a.half && k == 1) a.half[j] = (uint16_t)min(c, 0xffffu);
       }
       if (!fcount(r, x, stop, T, c)) bad = true;
     }
@@ -1641,17 +1591,9 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   // ahead, like its words
   uint32_t info_n = 0;
   int32_t dlt_n = 0;
-  uint32_t half_n = 0;  // dual-chain decode: first subsequence's count | second's gap byte << 16
-  const bool dual = VAR == BH_VARIANT_GAP && MODE == M_WIDE3 && a.half != nullptr;
-  auto half_load = [&](uint64_t t) -> uint32_t {
-    const uint64_t j = t * 32 + lane;
-    return (j < a.nsub) ? (uint32_t)a.half[j] | ((uint32_t)a.gap[2 * j + 1 < a.nsub_r ? 2 * j + 1 : 2 * j] << 16)
-                        : 0u;
-  };
   if (tile < t1) {
     info_n = a.lane_info[tile * 32 + lane];
     if (VAR == BH_VARIANT_SYNC) dlt_n = a.tile_dlt[tile];
-    if (dual) half_n = half_load(tile);
   }
   uint32_t dk = 0;  // tiles decoded (trace slots)
   if (MODE == M_WIDE3) mbar_wait(bar_dt, 0);  // the decode table has replaced c15
@@ -1659,11 +1601,9 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     const uint64_t tn = grab();
     const uint32_t info = info_n;
     const int32_t dlt = dlt_n;
-    const uint32_t half = half_n;
     if (tn < t1) {
       info_n = a.lane_info[tn * 32 + lane];
       if (VAR == BH_VARIANT_SYNC) dlt_n = a.tile_dlt[tn];
-      if (dual) half_n = half_load(tn);
     }
     uint32_t C, toff;
     if (srange) {
@@ -1730,17 +1670,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     if (fits && c) {
       SR r;
       r.init(base_s, e);
-      const uint32_t ca = half & 0xffffu;
-      // the lane's second subsequence (entered at its gap byte) as a second chain
-      const uint64_t j2 = 2 * (tile * 32 + lane) + 1;
-      if (dual && j2 < a.nsub_r && ca <= c) {
-        SR r2;
-        r2.init(base_s, b + a.sbr + (half >> 16));
-        const uint32_t d0 = stg_s + 2 * (sh + o);
-        if (!fdecode3_dual(r, ca, d0, r2, c - ca, d0 + 2 * ca, T)) bad = true;
-      } else if (!fdecode<MODE>(r, c, stg_s + 2 * (sh + o), T)) {
-        bad = true;
-      }
+      if (!fdecode<MODE>(r, c, stg_s + 2 * (sh + o), T)) bad = true;
     }
     __syncwarp();
     if (dk < 8) MARK(31 + 3 * dk);
@@ -1968,10 +1898,8 @@ static size_t class_freq_offset(const bh_stream* s) {
   return 64 + 16 * nseq_of(s) + 4 * 34 * nseq_of(s) + 64 * nseq_of(s) + 4 * nseq_of(s);
 }
 
-static size_t half_offset(const bh_stream* s) { return align16(class_freq_offset(s)) + 8 * TUNE_CLASSES; }
-
 extern "C" size_t bh_fused_workspace_bytes(const bh_stream* s, int, const bh_tune*) {
-  return align16(half_offset(s)) + 64 * nseq_of(s) + 256;
+  return align16(class_freq_offset(s)) + 8 * TUNE_CLASSES + 256;
 }
 
 // Which lanes form one reference sequence (tile = 32 lanes of spl subsequences):
@@ -2019,9 +1947,6 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.sps = TILE_SUBSEQ;
   a.spl = spl_of(s);
   a.sbr = s->subseq_bits;
-  a.half = (variant == BH_VARIANT_GAP && cfg.mode == M_WIDE3 && a.spl == 2 && !env_int("BH_FUSED_NODUAL", 0))
-               ? reinterpret_cast<uint16_t*>(static_cast<char*>(ws) + align16(half_offset(s)))
-               : nullptr;
   a.seq_bits = vsb_of(s) * TILE_SUBSEQ;
   a.tb = s->total_bits;
   a.nsym = s->symbol_count;
