@@ -43,8 +43,10 @@ def make_tune(capacity: int = DEFAULT_CAPACITY, tuner_config=None, collect_stats
 
 
 def run_decode(stream, variant: int, capacity: int = DEFAULT_CAPACITY, tuner_config=None,
-               stats=None, timings=None, return_device: bool = False, fused: bool | None = None):
-    t_enter = time.perf_counter()
+               stats=None, timings=None, return_device: bool = False, fused: bool | None = None,
+               t_enter: float | None = None):
+    if t_enter is None:
+        t_enter = time.perf_counter()
     torch = require_cuda()
     lib = load()
     ds = device_stream(stream)

@@ -8,6 +8,8 @@ in the same pass.  The sub-steps keep the reference's arrays.
 
 from __future__ import annotations
 
+import time
+
 import numpy as np
 
 from . import _lib
@@ -68,7 +70,8 @@ def count_pass(stream, state: SyncState, workers: int = 1, stats: DecodeStats | 
 def decode(stream, workers: int = 1, capacity: int = DEFAULT_CAPACITY, tuner_config=None,
            stats: DecodeStats | None = None, timings: dict | None = None, device_out: bool = False):
     """Decode a stream using its gap array; returns uint16 symbols."""
+    t_enter = time.perf_counter()  # timings cover the whole call
     if stream.gap is None:
         raise NotPresent("the stream carries no gap array")
     return run_decode(stream, _lib.VARIANT_GAP, capacity, tuner_config, stats, timings,
-                      return_device=device_out)
+                      return_device=device_out, t_enter=t_enter)

@@ -23,7 +23,7 @@ def ph():
 @pytest.fixture(scope="module")
 def field(ph):
     from paper_2201_09118_b200.synth import gaussian_codes
-    codes = gaussian_codes(3_000_000, 1024, 3.0, seed=2)
+    codes = gaussian_codes(12_000_000, 1024, 3.0, seed=2)
     return codes, ph.encode(codes, ph.book_for(codes, 16), ph.DEFAULT_LAYOUT, with_gap=True)
 
 
