@@ -1011,6 +1011,9 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
       if (!fcount(r, x, stop, T, c)) bad = true;
     }
     bool dprev = active;
+#ifdef BH_X_NOINTRA  // timing experiment only: no intra-sequence rounds (wrong output)
+    dprev = false;
+#endif
     while (true) {
       const uint32_t xin = __shfl_up_sync(0xffffffffu, x, 1);
       const bool din = __shfl_up_sync(0xffffffffu, dprev, 1);

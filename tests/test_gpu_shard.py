@@ -73,3 +73,23 @@ def test_decode_shard_single_symbol_book(variant):
         parts = sorted((o0, t.cpu().numpy().view(np.uint16)) for r in range(world)
                        for _, o0, t in shard.decode_shard([st], r, world, variant))
         assert np.array_equal(np.concatenate([p for _, p in parts]), codes)
+
+
+def test_decode_shard_refuses_layouts_the_fused_path_does_not_take():
+    """Chunks decode on the fused kernel only: a layout whose 32-lane tile
+    would exceed 16384 bits (subsequences of 1024 bits) is refused with a
+    clear error instead of a failed launch; whole-stream decodes of it still
+    work (staged pipeline)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2201_09118_b200 as ph
+    from paper_2201_09118_b200 import _lib, shard
+    from paper_2201_09118_b200.device import device_stream
+    from paper_2201_09118_b200.synth import gaussian_codes
+    codes = gaussian_codes(200_000, 1024, 3.0, seed=4)
+    st = ph.encode(codes, ph.book_for(codes, 16), ph.LayoutConfig(32, 32, 8), with_gap=True)
+    assert _lib.load().bh_fused_supported(device_stream(st).ref, _lib.VARIANT_GAP) == 0
+    with pytest.raises(ValueError, match="fused decoder"):
+        shard.decode_shard([st], 0, 2, "gap")
+    assert np.array_equal(ph.gap_decoder.decode(st), codes)
