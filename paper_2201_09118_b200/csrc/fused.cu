@@ -58,9 +58,6 @@ constexpr int kUnroll = BH_UNR;  // unroll of the tight count/decode loops
 #ifndef BH_CAPADD
 #define BH_CAPADD 96
 #endif
-#ifndef BH_X_LOCKSTEP
-#define BH_X_LOCKSTEP 0  // 1: intra-sequence re-decodes by the lock-step walk (A/B)
-#endif
 #ifndef BH_TWO
 #define BH_TWO 1  // two table lookups per bit-reader advance in the tight loops (HACC gap -5% time)
 #endif
@@ -596,57 +593,6 @@ __device__ __forceinline__ bool resync_step(uint32_t base_s, uint32_t eo, uint32
   }
 }
 
-// Re-decode from a new entry for the wide modes, branch-light: both parses
-// advance one codeword per iteration (instead of whichever lags, a choice
-// that splits the warp into two paths), their starts within 64 bits of the
-// old entry are marked in two masks, and the lowest common start is where
-// they meet (from there they coincide).  Counts come from the masks; a meet
-// farther than 64 bits finishes with the lock-step walk.
-template <int MODE>
-__device__ __forceinline__ bool resync_bits(uint32_t base_s, uint32_t eo, uint32_t co, uint32_t xo, uint32_t en,
-                                            uint32_t stop, const FTab& T, uint32_t& cn, uint32_t& xn) {
-  if (en >= stop) { cn = 0; xn = en; return true; }
-  if (en < eo || en - eo >= 64) return resync_step<MODE>(base_s, eo, co, xo, en, stop, T, cn, xn);
-  const uint32_t sn = stop - eo;  // window end, relative to eo
-  uint32_t po = 0, pn = en - eo;
-  unsigned long long mo = 0, mn = 0;
-  // position-only readers (two word loads per peek): two full bit readers
-  // would not fit the register budget next to the sequence state
-  auto peek_at = [&](uint32_t p) -> uint32_t {
-    const uint32_t j = p >> 5;
-    return __funnelshift_l(lds32(skew_addr(base_s, j + 1)), lds32(skew_addr(base_s, j)), p & 31);
-  };
-  while (true) {
-    if (po < 64) mo |= 1ull << po;
-    if (pn < 64) mn |= 1ull << pn;
-    const unsigned long long both = mo & mn;
-    if (both) {  // they meet at the lowest common start m (< the window end: checked below first)
-      const unsigned long long below = (both & (0ull - both)) - 1ull;
-      cn = (uint32_t)__popcll(mn & below) + co - (uint32_t)__popcll(mo & below);
-      xn = xo;
-      return true;
-    }
-    if (pn >= sn) {  // the new parse left the window first: its codewords and exit
-      cn = (uint32_t)__popcll(mn & ((sn < 64 ? (1ull << sn) : 0ull) - 1ull));
-      xn = eo + pn;
-      return true;
-    }
-    if (po >= 64 || pn >= 64) {  // far meet: lock-step from here
-      const uint32_t no = po < 64 ? (uint32_t)__popcll(mo & ((1ull << po) - 1ull)) : (uint32_t)__popcll(mo);
-      const uint32_t nn = (uint32_t)__popcll(mn) - (pn < 64 ? 1u : 0u);
-      uint32_t c2, x2;
-      if (!resync_step<MODE>(base_s, eo + po, co - no, xo, eo + pn, stop, T, c2, x2)) return false;
-      cn = nn + c2;
-      xn = x2;
-      return true;
-    }
-    const uint32_t lo = clen<MODE>(peek_at(eo + po), T), ln = clen<MODE>(peek_at(eo + pn), T);
-    if (!lo || !ln) return false;
-    po += lo;
-    pn += ln;
-  }
-}
-
 template <int MODE>
 __device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co, uint32_t xo, uint32_t en,
                                        uint32_t stop, const FTab& T, uint32_t& cn, uint32_t& xn) {
@@ -1076,9 +1022,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
       bool dnow = false;
       if (live && xin != e) {
         uint32_t cn, xn;
-        if (!(MODE != M_NARROW && !BH_X_LOCKSTEP ? resync_bits<MODE>(base_s, e, c, x, xin, stop, T, cn, xn)
-                                                 : resync<MODE>(base_s, e, c, x, xin, stop, T, cn, xn)))
-          bad = true;
+        if (!resync<MODE>(base_s, e, c, x, xin, stop, T, cn, xn)) bad = true;
         e = xin;
         c = cn;
         x = xn;
@@ -1149,9 +1093,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
           bool dnow = false;
           if (live && xin != e) {
             uint32_t cn, xn;
-            if (!(MODE != M_NARROW && !BH_X_LOCKSTEP ? resync_bits<MODE>(base_s, e, c, x, xin, stop, T, cn, xn)
-                                                 : resync<MODE>(base_s, e, c, x, xin, stop, T, cn, xn)))
-          bad = true;
+            if (!resync<MODE>(base_s, e, c, x, xin, stop, T, cn, xn)) bad = true;
             e = xin;
             c = cn;
             x = xn;
