@@ -233,6 +233,14 @@ def ingest_shard(path, rank: int = 0, world: int = 1, variant: str = "gap", devi
     nsub = -(-info.total_bits // sb)
     nseq = -(-nsub // sps)
     q0, q1 = sequence_ranges(nseq, world)[rank]
+    if q0 >= q1:  # more ranks than sequences: this rank holds nothing
+        n, out0, total = 0, None, 0
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            from .shard import gather_totals, shard_offsets
+            totals = gather_totals(0, group)
+            out0, total = shard_offsets(totals)[rank], sum(totals)
+        return torch.empty(0, dtype=torch.int16, device=dev), out0, total
     s0, s1 = q0 * sps, min(q1 * sps, nsub)
     b0 = q0 * sb * sps
     stager = _Stager(torch, dev, CHUNK_BYTES)

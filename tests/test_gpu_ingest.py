@@ -60,3 +60,16 @@ def test_large_file_and_shards(ph, tmp_path, unit_bits, ups):
         ingest.ingest_shard(path, 0, 1, "gap")
     with pytest.raises(ph.BadGap):
         ingest.decode_container(path, "gap")
+
+
+def test_shards_with_more_ranks_than_sequences(ph, tmp_path):
+    from paper_2201_09118_b200 import ingest
+    from paper_2201_09118_b200.synth import gaussian_codes
+    codes = gaussian_codes(3000, 1024, 8.0, seed=5)
+    st = ph.encode(codes, ph.book_for(codes, 16), ph.DEFAULT_LAYOUT, with_gap=True)
+    path = tmp_path / "small.huf2"
+    ph.write_container(st, path)
+    world = st.num_seqs + 3
+    parts = [ingest.ingest_shard(path, r, world, v)[0] for v in ("gap",) for r in range(world)]
+    cat = np.concatenate([p.cpu().numpy().view(np.uint16) for p in parts])
+    assert np.array_equal(cat, codes)
