@@ -335,7 +335,21 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
     // 15 bits per lookup, two lookups per advance; the window end and codes
     // longer than 15 bits fall through to the 12-bit loop below
     const uint32_t c5 = pin(T.c15);
+    // bulk: two lookups (<= 30 bits) cannot cross `stop`; an empty second
+    // entry (code longer than 15 bits after the first) adds nothing
+    const int32_t bulk_end = (int32_t)stop - 2 * C15;
 #pragma unroll (kUnroll)
+    while ((int32_t)pos <= bulk_end) {
+      const uint32_t win = r.peek();
+      const uint32_t y = lds8(c5 + (win >> (32 - C15)));
+      if (y == 0) break;
+      const uint32_t y2 = lds8(c5 + ((win << (y >> 4)) >> (32 - C15)));
+      n += (y & 15u) + (y2 & 15u);
+      const uint32_t adv = (y >> 4) + (y2 >> 4);
+      r.skip(adv);
+      pos += adv;
+    }
+#pragma unroll 1
     while (true) {
       const uint32_t win = r.peek();
       const uint32_t y = lds8(c5 + (win >> (32 - C15)));
@@ -354,6 +368,23 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
     // tight loop: whole entries that end at or before the window end (one
     // extra lookup when an entry ends exactly at it)
     uint32_t y, b;
+#if BH_TWO
+    {
+      // bulk: two lookups (<= 24 bits) cannot cross `stop`
+      const int32_t bulk_end = (int32_t)stop - 2 * FB;
+#pragma unroll (kUnroll)
+      while ((int32_t)pos <= bulk_end) {
+        const uint32_t win = r.peek();
+        const uint32_t y1 = lds16(ct + ((win >> (32 - FB)) << 1));
+        if (y1 == 0) break;
+        const uint32_t y2 = lds16(ct + (((win << (y1 >> 12)) >> (32 - FB)) << 1));
+        n += __popc(y1 & 0xfffu) + __popc(y2 & 0xfffu);
+        const uint32_t adv = (y1 >> 12) + (y2 >> 12);
+        r.skip(adv);
+        pos += adv;
+      }
+    }
+#endif
 #pragma unroll (kUnroll)
     while (true) {
 #if BH_TWO
@@ -400,6 +431,14 @@ __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, cons
   return true;
 }
 
+// idx * 8 + base as one integer multiply-add (the compiler would otherwise
+// fold the shift into a mask and add: three ALU instructions)
+__device__ __forceinline__ uint32_t mad8(uint32_t idx, uint32_t base) {
+  uint32_t a;
+  asm("mad.lo.u32 %0, %1, 8, %2;" : "=r"(a) : "r"(idx), "r"(base));
+  return a;
+}
+
 // Decode c (>= 1) symbols into compact staging at `dst`.  While at least six
 // symbols remain, all six symbols of a table entry are stored unconditionally
 // (the ones past the entry's count land inside the lane's own range and are
@@ -420,30 +459,26 @@ __device__ __forceinline__ bool fdecode3(SR& r, uint32_t c, uint32_t dst, const 
 #pragma unroll (kUnroll)
     while (k2 >= 16) {
       const uint32_t win = r.peek();
-      const uint2 e = lds64(wl + ((win >> (32 - FB)) << 3));
+      const uint2 e = lds64(mad8(win >> (32 - FB), wl));
       if (!e.y) break;
       const uint32_t b1 = (e.y >> 24) & 15u;
-      const uint2 f = lds64(wl + (((win << b1) >> (32 - FB)) << 3));
+      const uint2 f = lds64(mad8((win << b1) >> (32 - FB), wl));
       uint32_t odd = dst & 2u, a4 = dst + odd;
       sts16(dst, e.x);
       sts32(a4, __funnelshift_r(e.x, e.y, odd << 3));
       sts32(a4 + 4, e.y);
-      const uint32_t nb1 = e.y >> 28;
-      dst += nb1;
-      uint32_t adv = b1, nb = nb1;
-      if (f.y) {
-        odd = dst & 2u;
-        a4 = dst + odd;
-        sts16(dst, f.x);
-        sts32(a4, __funnelshift_r(f.x, f.y, odd << 3));
-        sts32(a4 + 4, f.y);
-        const uint32_t nb2 = f.y >> 28;
-        dst += nb2;
-        nb += nb2;
-        adv += (f.y >> 24) & 15u;
-      }
-      k2 -= (int32_t)nb;
-      r.skip(adv);
+      dst += e.y >> 28;
+      // the second entry unconditionally: a long code there (f.y == 0) writes
+      // zero-length junk inside the lane's range and advances nothing
+      odd = dst & 2u;
+      a4 = dst + odd;
+      sts16(dst, f.x);
+      sts32(a4, __funnelshift_r(f.x, f.y, odd << 3));
+      sts32(a4 + 4, f.y);
+      const uint32_t nb2 = f.y >> 28;
+      dst += nb2;
+      k2 -= (int32_t)((e.y >> 28) + nb2);
+      r.skip(b1 + ((f.y >> 24) & 15u));
     }
 #endif
 #pragma unroll (kUnroll)
