@@ -58,6 +58,12 @@ constexpr int kUnroll = BH_UNR;  // unroll of the tight count/decode loops
 #ifndef BH_CAPADD
 #define BH_CAPADD 96
 #endif
+#ifndef BH_REV
+#define BH_REV 1  // phase 2 walks the range backwards: the tiles counted last are still in L2
+#endif
+#ifndef BH_L2HINT
+#define BH_L2HINT 2  // 1: output bulk stores evict_first; 2: also the decode phase's word reads (their last use)
+#endif
 #ifndef BH_TWO
 #define BH_TWO 1  // two table lookups per bit-reader advance in the tight loops (HACC gap -5% time)
 #endif
@@ -735,6 +741,16 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void* src, uint32_t
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                ::"r"(dst), "l"(src), "r"(bytes), "r"(bar) : "memory");
 }
+__device__ __forceinline__ uint64_t l2_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void bulk_g2s_hint(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar,
+                                              uint64_t pol) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;"
+               ::"r"(dst), "l"(src), "r"(bytes), "r"(bar), "l"(pol) : "memory");
+}
 __device__ __forceinline__ void sts128(uint32_t a, uint4 v) {
   asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
 }
@@ -763,7 +779,7 @@ __device__ __forceinline__ void wstage_init(WStage& ws, uint32_t bar) {
 // Stage the words of `tile`; returns the bit offset of logical word 0.  The
 // caller has synced the warp after its last read of the landing buffer.
 __device__ __forceinline__ uint64_t stage_words(const FusedArgs& a, uint64_t tile, uint32_t land_s, uint32_t& nch,
-                                                WStage& ws) {
+                                                WStage& ws, bool last_use = false) {
   const uint64_t s0 = tile * (uint64_t)a.seq_bits;
   const uint64_t w0 = (s0 >> 5) & ~3ull;
   uint64_t w1 = ((s0 + a.seq_bits) >> 5) + HALO_WORDS;
@@ -774,7 +790,8 @@ __device__ __forceinline__ uint64_t stage_words(const FusedArgs& a, uint64_t til
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier reads of the buffer -> async proxy
     if (nch) {
       mbar_expect_tx(ws.bar, 16 * nch);
-      bulk_g2s(land_s, a.words + w0, 16 * nch, ws.bar);
+      if (BH_L2HINT >= 2 && last_use) bulk_g2s_hint(land_s, a.words + w0, 16 * nch, ws.bar, l2_evict_first());
+      else bulk_g2s(land_s, a.words + w0, 16 * nch, ws.bar);
     } else {
       mbar_arrive(ws.bar);
     }
@@ -862,9 +879,14 @@ __device__ __forceinline__ bool flush_bulk(uint16_t* __restrict__ out, uint64_t 
   const bool bulk = f1 > f0;
   if (bulk && lane == 0) {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // staging stores -> async proxy
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
-                 ::"l"(out + f0), "r"(stg_s + 2 * (uint32_t)(f0 - a0)), "r"((uint32_t)(2 * (f1 - f0)))
-                 : "memory");
+    if (BH_L2HINT >= 1)  // the output is not read again: keep the payload in L2 instead
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group.L2::cache_hint [%0], [%1], %2, %3;"
+                   ::"l"(out + f0), "r"(stg_s + 2 * (uint32_t)(f0 - a0)), "r"((uint32_t)(2 * (f1 - f0))),
+                   "l"(l2_evict_first()) : "memory");
+    else
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                   ::"l"(out + f0), "r"(stg_s + 2 * (uint32_t)(f0 - a0)), "r"((uint32_t)(2 * (f1 - f0)))
+                   : "memory");
     asm volatile("cp.async.bulk.commit_group;" ::: "memory");
   }
   const uint64_t hend = f0 < g1 ? f0 : g1;
@@ -1615,15 +1637,18 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   // ---- phase 2: decode and write -----------------------------------------
   // tiles are taken dynamically (a shared counter): a warp that finishes
   // early takes the next tile, so the range's last round is balanced
-  tile = t0 + wib;
+  // (BH_REV: from the end of the range, whose words the count phase read
+  // last and L2 still holds; t1 marks the end either way)
+  auto pick = [&](uint32_t v) -> uint64_t { return v < nt ? (BH_REV ? t1 - 1 - v : t0 + v) : t1; };
+  tile = pick(wib);
   __syncwarp();
-  if (tile < t1) wb_a = stage_words(a, tile, land_s, nch_a, wst);
+  if (tile < t1) wb_a = stage_words(a, tile, land_s, nch_a, wst, true);
   bool have_off = false, bulk_pending = false;
   unsigned long long Pc = 0;
   auto grab = [&]() -> uint64_t {
     uint32_t v = 0;
     if (lane == 0) v = atomicAdd(&s_next, 1u);
-    return t0 + __shfl_sync(0xffffffffu, v, 0);
+    return pick(__shfl_sync(0xffffffffu, v, 0));
   };
   // the tile's lane info (entry, prefix) and seam delta are loaded one tile
   // ahead, like its words
@@ -1658,7 +1683,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     if (dk < 8) MARK(30 + 3 * dk);
     skew_in(land_s, dbuf_s, nch_a);
     __syncwarp();
-    if (tn < t1) wb_b = stage_words(a, tn, land_s, nch_b, wst);  // lands while this tile decodes
+    if (tn < t1) wb_b = stage_words(a, tn, land_s, nch_b, wst, true);  // lands while this tile decodes
     const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
     const uint32_t base_s = dbuf_s;
     const uint32_t b = (uint32_t)((tile * a.sps + lane) * a.sb - wb_a);
