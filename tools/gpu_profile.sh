@@ -13,7 +13,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
     python bench.py --steps 5 --warmup 3 --no-cpu-baseline > $O/launches_bench.log 2>&1
 for v in gap sync; do
   ncu --set full --clock-control none --import-source on -k regex:k_fused -s 4 -c 1 -f -o $O/fused_$v \
-      python bench.py --steps 3 --warmup 3 --no-extras --no-cpu-baseline --graph 0 --variant $v > $O/ncu_$v.log 2>&1
+      python bench.py --steps 3 --warmup 3 --no-extras --no-cpu-baseline --variant $v > $O/ncu_$v.log 2>&1
 done
 bash tools/quick.sh 1m hurricane hurricane:sync nyx nyx256 nyx4096 hacc hacc:sync qmcpack cesm rtm > $O/quick.txt 2>&1
 python bench.py --config multifield --steps 20 --warmup 3 > $O/bench_multifield.json 2> $O/bench_multifield.err

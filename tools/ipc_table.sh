@@ -7,7 +7,7 @@ O=gpurun_out/ipc; mkdir -p $O
 CFGS="$*"
 [ -z "$CFGS" ] && CFGS="hurricane nyx256 nyx nyx4096 hacc cesm rtm qmcpack hurricane:sync nyx:sync hacc:sync cesm:sync rtm:sync qmcpack:sync"
 M=smsp__inst_executed.sum,gpu__time_duration.sum,sm__inst_executed.avg.per_cycle_active,smsp__issue_active.avg.pct_of_peak_sustained_active,smsp__thread_inst_executed_per_inst_executed.ratio,dram__bytes_read.sum,dram__bytes_write.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum,l1tex__data_pipe_lsu_wavefronts_mem_shared.sum
-printf "%-10s %-4s %11s %9s %10s %6s %6s %6s %9s %9s %6s\n" config var symbols time_us warp_inst inst/sym IPC issue% thr_eff dram_rd_MB dram_wr_MB conf%
+printf "%-10s %-4s %11s %9s %10s %6s %6s %6s %9s %9s %9s %6s\n" config var symbols time_us warp_inst inst/sym IPC issue% thr_eff dram_rd_MB dram_wr_MB conf%
 for c in $CFGS; do
   v=gap; cfg=$c
   case $c in *:sync) v=sync; cfg=${c%:sync};; esac
@@ -28,7 +28,7 @@ for r in rows[1:]:
         v = float(d["Metric Value"].replace(",", ""))
         u = d.get("Metric Unit", "")
         if d["Metric Name"] == "gpu__time_duration.sum":
-            v = v / 1e3 if u == "nsecond" else v * 1e3 if u == "msecond" else v
+            v = v / 1e3 if u in ("ns", "nsecond") else v * 1e3 if u in ("ms", "msecond") else v
         v *= {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u, 1.0)
         m[d["Metric Name"]] = v
 n = synth.FIELDS[sys.argv[2]].n
