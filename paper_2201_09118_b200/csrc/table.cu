@@ -370,6 +370,13 @@ __device__ __forceinline__ void pack6(uint32_t& x, uint32_t& y, uint32_t& z, uin
   if (k < 2) x |= v; else if (k < 4) y |= v; else z |= v;
 }
 
+#ifdef BH_K1_STAMPS
+__device__ unsigned long long g_k1_stamps[8];
+#define K1ST(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_k1_stamps[k] = global_ns(); } while (0)
+#else
+#define K1ST(k) do { } while (0)
+#endif
+
 __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __restrict__ lengths, uint32_t alphabet,
                                                            void* blob, uint32_t max_codes) {
   __shared__ CanonSmem S;
@@ -380,12 +387,14 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   if (tid < 33) { S.count[tid] = 0; S.fill[tid] = 0; }
   if (tid == 0) S.bad = 0;
   __syncthreads();
+  K1ST(0);
   for (uint32_t s = tid; s < alphabet; s += K1_THREADS) {
     const uint32_t ln = lengths[s];
     if (ln > 32) S.bad = 1;
     else if (ln) atomicAdd(&S.count[ln], 1u);
   }
   __syncthreads();
+  K1ST(1);
   // first_code / first_index per length (codebook.py:209-233) as one warp scan:
   // lane ln-1 holds count c and its left-justified Kraft share d = c << (32-ln);
   // the exclusive prefix of d is first_code << (32-ln) exactly, and its
@@ -437,6 +446,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
     }
   }
   __syncthreads();
+  K1ST(2);
   if (S.bad) return;
   // ranks: counting sort by (length, symbol).  Per 1024-symbol block: a
   // symbol's rank among its warp's peers (match_any), the peers in earlier
@@ -478,14 +488,36 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
       }
     }
     __syncthreads();
+  K1ST(3);
   }
-  // every codeword of <= 12 bits by its 12-bit prefix (one limit search per
-  // entry, in every CTA); the direct tables then walk windows through it
-  for (uint32_t v = tid; v < FB_SIZE; v += K1_THREADS) {
-    const uint32_t e = canon_one(S, v << (32 - FB));
-    S.l12[v] = ((e >> 16) & 0xffu) <= (uint32_t)FB ? e : 0u;
+  // every codeword of <= 12 bits by its 12-bit prefix, in every CTA; the
+  // direct tables then walk windows through it.  The length at a prefix is 1
+  // + the number of limits at or below it (the limits of lengths 1..12 held
+  // in registers, clamped to 32 bits: a prefix window's low 20 bits are zero,
+  // so it never reaches 0xffffffff) -- twelve independent compares instead
+  // of a dependent limit search
+  {
+    uint32_t lc[FB];
+#pragma unroll
+    for (int k = 0; k < FB; ++k) {
+      const unsigned long long l = S.lim[k + 1];
+      lc[k] = l > 0xffffffffull ? 0xffffffffu : (uint32_t)l;
+    }
+    for (uint32_t v = tid; v < FB_SIZE; v += K1_THREADS) {
+      const uint32_t w = v << (32 - FB);
+      uint32_t ln = 1;
+#pragma unroll
+      for (int k = 0; k < FB; ++k) ln += w >= lc[k] ? 1u : 0u;
+      uint32_t e = 0;
+      if (ln <= (uint32_t)FB) {
+        const long long idx = S.base[ln] + (long long)(w >> (32 - ln));
+        e = (uint32_t)S.sym[idx] | (ln << 16);
+      }
+      S.l12[v] = e;
+    }
   }
   __syncthreads();
+  K1ST(4);
   // direct tables: 12-bit (lut12, clut12, wlut12, wlut12n), 11-bit (lut, cnt)
   // and 8-bit (dlut8, clut8, wlut8) entries spread over every thread of the
   // grid.  A codeword at offset pos of a W-bit window v is S.l12 of the 12
@@ -505,6 +537,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   // (built for books whose codes are all >= 4 bits -- the only ones the
   // fused kernel counts with it -- and all zero, "use the 12-bit table",
   // otherwise)
+  K1ST(5);
   uint8_t* c15 = reinterpret_cast<uint8_t*>(B + L.c15);
   const bool build15 = S.minl >= 4;
   for (uint32_t v = cta * K1_THREADS + tid; v < (uint32_t)C15_SIZE; v += G * K1_THREADS) {
@@ -565,6 +598,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
       wlut8[v] = wl;
     }
   }
+  K1ST(6);
 }
 
 }  // namespace bh
@@ -575,12 +609,23 @@ static int cuda_status(cudaError_t e) { return e == cudaSuccess ? BH_OK : BH_CUD
 
 extern "C" size_t bh_table_bytes(uint32_t max_codes) { return TableLayout(max_codes).total; }
 
+#ifdef BH_K1_STAMPS
+extern "C" int bh_debug_k1_stamps(unsigned long long* host8) {
+  return cudaMemcpyFromSymbol(host8, bh::g_k1_stamps, 64) == cudaSuccess ? BH_OK : BH_CUDA_ERROR;
+}
+#endif
+
 extern "C" int bh_table_build(const uint8_t* lengths_dev, uint32_t alphabet, void* table_dev,
                               uint32_t max_codes, void* cuda_stream) {
   if (!table_dev || (alphabet && !lengths_dev) || alphabet > 65536u || max_codes > 65536u)
     return BH_BAD_ARGUMENT;
   cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-  k_table_canon<<<K1_GRID, K1_THREADS, 0, st>>>(lengths_dev, alphabet, table_dev, max_codes);
+  static const int grid = [] {
+    const char* e = getenv("BH_K1_GRID");  // tuning knob
+    const int g = e && *e ? atoi(e) : 0;
+    return g > 0 && g <= 148 ? g : K1_GRID;
+  }();
+  k_table_canon<<<grid, K1_THREADS, 0, st>>>(lengths_dev, alphabet, table_dev, max_codes);
   return cuda_status(cudaGetLastError());
 }
 
