@@ -1270,6 +1270,10 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       a.trace[((size_t)blockIdx.x * a.warps + (threadIdx.x >> 5)) * TRACE_SLOTS + (slot)] = gtime(); \
   } while (0)
   MARK(0);
+  // launched with programmatic stream serialisation: the CTAs start while the
+  // preceding kernel (normally K1, which builds the tables) drains; nothing
+  // it writes is read before this wait
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   extern __shared__ __align__(16) unsigned char sm[];
   // mbarriers: [0] count tables (c12, lim, base), [1] decode tables (wlut8,
   // lut12), [2] CTA output offset published (1 arrival)
@@ -2116,9 +2120,17 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   if (grid < 1) grid = 1;
   prof_mark(static_cast<cudaStream_t>(cuda_stream), "start");
   void* args[] = {&a};
-  if (cudaLaunchKernel(fn, dim3((unsigned)grid), dim3(cfg.warps * 32), args, cfg.smem,
-                       static_cast<cudaStream_t>(cuda_stream)) != cudaSuccess)
-    return BH_CUDA_ERROR;
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = dim3((unsigned)grid);
+  lc.blockDim = dim3(cfg.warps * 32);
+  lc.dynamicSmemBytes = cfg.smem;
+  lc.stream = static_cast<cudaStream_t>(cuda_stream);
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = env_int("BH_PDL", 1) ? 1 : 0;
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  if (cudaLaunchKernelExC(&lc, fn, args) != cudaSuccess) return BH_CUDA_ERROR;
   prof_mark(static_cast<cudaStream_t>(cuda_stream), variant == BH_VARIANT_GAP ? "fused_gap" : "fused_sync");
   return cudaGetLastError() == cudaSuccess ? BH_OK : BH_CUDA_ERROR;
 }

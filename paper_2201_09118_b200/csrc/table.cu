@@ -380,6 +380,9 @@ __device__ unsigned long long g_k1_stamps[8];
 __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __restrict__ lengths, uint32_t alphabet,
                                                            void* blob, uint32_t max_codes) {
   __shared__ CanonSmem S;
+  // the decode kernel that follows may launch now (its CTAs wait for this
+  // grid's completion before reading the tables)
+  asm volatile("griddepcontrol.launch_dependents;");
   TableHdr* hdr; uint32_t* lut; uint16_t* cnt; uint32_t* lj; uint16_t* ljsym; uint8_t* ljlen;
   table_ptrs(blob, max_codes, hdr, lut, cnt, lj, ljsym, ljlen);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
