@@ -383,6 +383,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   // the decode kernel that follows may launch now (its CTAs wait for this
   // grid's completion before reading the tables)
   asm volatile("griddepcontrol.launch_dependents;");
+  K1ST(7);
   TableHdr* hdr; uint32_t* lut; uint16_t* cnt; uint32_t* lj; uint16_t* ljsym; uint8_t* ljlen;
   table_ptrs(blob, max_codes, hdr, lut, cnt, lj, ljsym, ljlen);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;

@@ -28,4 +28,5 @@ for name in ("hurricane", "hacc", "nyx4096"):
     buf = (C.c_ulonglong * 8)()
     lib.bh_debug_k1_stamps(buf)
     s = list(buf)
-    print(name, "  ".join(f"{names[k]} {(s[k] - s[k - 1]) / 1e3:.2f}us" for k in range(1, 7)), f"total {(s[6] - s[0]) / 1e3:.2f}us")
+    print(name, f"entry->init {(s[0] - s[7]) / 1e3:.2f}us ", "  ".join(f"{names[k]} {(s[k] - s[k - 1]) / 1e3:.2f}us" for k in range(1, 7)),
+          f"total {(s[6] - s[7]) / 1e3:.2f}us")
