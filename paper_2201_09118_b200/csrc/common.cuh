@@ -62,14 +62,16 @@ struct TableHdr {
 //   lut12 u32[4096]  next 12 bits -> sym | len<<16 for codes of <= 12 bits, else 0
 //   wlut12 uint4[4096] next 12 bits -> up to 6 whole codewords, wlut8's format
 //                    (the fused kernels' decode table for long-code books)
-//   wlut12n uint2[4096] next 12 bits -> up to 3 whole codewords in 8 bytes (the
+//   wlut3 uint2[8192] next 13 bits -> up to 3 whole codewords in 8 bytes (the
 //                    fused kernels' decode table for books whose codes are all
-//                    >= 4 bits, so no 12-bit window holds more than three):
+//                    >= 4 bits, so no 13-bit window holds more than three):
 //                    x = s0 | s1<<16, y = s2 | len0<<16 | bits<<24 | 2n<<28
-//                    (y == 0: the first code is longer than 12 bits)
-//   c15   u8[32768]  next 15 bits -> n | bits<<4 over every whole codeword of the
-//                    window (n, bits <= 15); 0 if the first one is longer
-//                    (the count phase of the long-code fused decoders)
+//                    (y == 0: the first code is longer than 12 bits or ends
+//                    past the window)
+//   cwin  u8[65536]  next 16 bits -> n | bits<<3 over every whole codeword of
+//                    the window (n <= 4, bits <= 16); 0 if the first one is
+//                    longer (the count phase of the long-code fused decoders;
+//                    built for books whose codes are all >= 4 bits)
 //   len12 u8[4096]   next 12 bits -> length of the first codeword if <= 12 bits, else 0
 //                    (the self-sync decoders' per-codeword resynchronization walk)
 //   clut12 u16[4096] next 12 bits -> starts | bits<<12 over every whole codeword
@@ -82,13 +84,15 @@ struct TableHdr {
 // ever touches shared-memory bank l), so table lookups never conflict.
 constexpr int FB = 12;
 constexpr int FB_SIZE = 1 << FB;
-constexpr int C15 = 15;  // count-table window of the long-code fused path
-constexpr int C15_SIZE = 1 << C15;
+constexpr int D3 = 13;  // window of the three-codeword decode table (wlut3)
+constexpr int D3_SIZE = 1 << D3;
+constexpr int CW = 16;  // window of the count table of the long-code fused path (cwin)
+constexpr int CW_SIZE = 1 << CW;
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
 
 struct TableLayout {
-  size_t lut, cnt, dlut8, clut8, wlut8, lut12, clut12, wlut12, wlut12n, c15, len12, lim, base, lj, ljsym, ljlen, total;
+  size_t lut, cnt, dlut8, clut8, wlut8, lut12, clut12, wlut12, wlut3, cwin, len12, lim, base, lj, ljsym, ljlen, total;
   __host__ __device__ explicit TableLayout(uint32_t max_codes) {
     lut = TABLE_HDR_BYTES;
     cnt = lut + sizeof(uint32_t) * LUT_SIZE;
@@ -98,9 +102,9 @@ struct TableLayout {
     lut12 = align16(wlut8 + 16 * 256);
     clut12 = lut12 + 4 * (size_t)FB_SIZE;
     wlut12 = align16(clut12 + 2 * (size_t)FB_SIZE);
-    wlut12n = align16(wlut12 + 16 * (size_t)FB_SIZE);
-    c15 = align16(wlut12n + 8 * (size_t)FB_SIZE);
-    len12 = align16(c15 + (size_t)C15_SIZE);
+    wlut3 = align16(wlut12 + 16 * (size_t)FB_SIZE);
+    cwin = align16(wlut3 + 8 * (size_t)D3_SIZE);
+    len12 = align16(cwin + (size_t)CW_SIZE);
     lim = align16(len12 + (size_t)FB_SIZE);
     base = lim + 8 * 33;
     lj = align16(base + 8 * 33);

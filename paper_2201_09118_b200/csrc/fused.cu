@@ -145,11 +145,11 @@ constexpr unsigned long long FUSED_MARK = 0xF05EDull;  // rep->pad[2]: report wr
 constexpr uint32_t T_LIMBASE = 2 * 33 * 8;  // lim u64[33], base i64[33] (contiguous)
 constexpr uint32_t T_NARROW_DEC = 256 * 8 * 16;
 constexpr uint32_t T_WIDE_DEC = 16 * FB_SIZE;
-constexpr uint32_t T_WIDE3_DEC = 8 * FB_SIZE;
+constexpr uint32_t T_WIDE3_DEC = 8 * D3_SIZE;  // also holds cwin (CW_SIZE) in phase 1
 // Decode-table modes (template parameter MODE of the kernel):
 //   M_NARROW -- 8-bit window, up to six codewords, 16-byte entries replicated 8 ways;
 //   M_WIDE   -- 12-bit window, up to six codewords, 16-byte entries (wlut12);
-//   M_WIDE3  -- 12-bit window, up to three codewords, 8-byte entries (wlut12n),
+//   M_WIDE3  -- 13-bit window, up to three codewords, 8-byte entries (wlut3),
 //               for books whose codes are all >= 4 bits: half the table, half
 //               the shared-memory wavefronts per lookup and no store predicates.
 constexpr int M_NARROW = 0, M_WIDE = 1, M_WIDE3 = 2;
@@ -261,7 +261,7 @@ struct FTab {
   uint32_t dst;    // entry stride shift: 7 (8 replicas x 16 B) or 4 (16 B)
   uint32_t l12;    // shared address of lut12
   uint32_t c12;    // shared address of clut12
-  uint32_t c15;    // shared address of the 15-bit count table (phase 1 of M_WIDE3; 0 = none)
+  uint32_t cw;     // shared address of the 16-bit count table cwin (phase 1 of M_WIDE3; 0 = none)
   uint32_t len12;  // shared address of len12 (wide modes: first codeword length, resync walk)
   uint32_t ljs;    // shared address of the canonical symbol order (0: read it from global)
   uint32_t lim;    // shared address of lim (u64[33])
@@ -302,7 +302,7 @@ __device__ __forceinline__ uint32_t flong(uint32_t win, const FTab& T) {
 template <int MODE>
 __device__ __forceinline__ uint32_t fone(uint32_t win, const FTab& T) {
   if (MODE == M_WIDE3) {
-    const uint2 e = lds64(T.wl + ((win >> (32 - FB)) << 3));
+    const uint2 e = lds64(T.wl + ((win >> (32 - D3)) << 3));
     if (e.y) return (e.x & 0xffffu) | (((e.y >> 16) & 31u) << 16);
     return flong(win, T);
   }
@@ -336,35 +336,36 @@ __device__ __forceinline__ uint32_t clen(uint32_t win, const FTab& T) {
 // than 12 bits takes one codeword.
 __device__ __forceinline__ bool fcount(SR& r, uint32_t& pos, uint32_t stop, const FTab& T, uint32_t& n) {
   const uint32_t ct = pin(T.c12);
-  if (T.c15) {
-    // 15-bit count table (M_WIDE3 phase 1): every whole codeword of the next
-    // 15 bits per lookup, two lookups per advance; the window end and codes
-    // longer than 15 bits fall through to the 12-bit loop below
-    const uint32_t c5 = pin(T.c15);
-    // bulk: two lookups (<= 30 bits) cannot cross `stop`; an empty second
-    // entry (code longer than 15 bits after the first) adds nothing
-    const int32_t bulk_end = (int32_t)stop - 2 * C15;
+  if (T.cw) {
+    // 16-bit count table (M_WIDE3 phase 1): every whole codeword of the next
+    // 16 bits per lookup (n | bits<<3), two lookups per advance; the window
+    // end and codes longer than 16 bits fall through to the 12-bit loop below
+    const uint32_t c5 = pin(T.cw);
+    // bulk: two lookups (<= 32 bits) cannot cross `stop`; an empty second
+    // entry (code longer than 16 bits after the first) adds nothing
+    const int32_t bulk_end = (int32_t)stop - 2 * CW;
 #pragma unroll (kUnroll)
     while ((int32_t)pos <= bulk_end) {
       const uint32_t win = r.peek();
-      const uint32_t y = lds8(c5 + (win >> (32 - C15)));
+      const uint32_t y = lds8(c5 + (win >> (32 - CW)));
       if (y == 0) break;
-      const uint32_t y2 = lds8(c5 + ((win << (y >> 4)) >> (32 - C15)));
-      n += (y & 15u) + (y2 & 15u);
-      const uint32_t adv = (y >> 4) + (y2 >> 4);
+      const uint32_t b = y >> 3;
+      const uint32_t y2 = lds8(c5 + ((win << b) >> (32 - CW)));  // b <= 16: the next 16 bits lie in win
+      n += (y & 7u) + (y2 & 7u);
+      const uint32_t adv = b + (y2 >> 3);
       r.skip(adv);
       pos += adv;
     }
 #pragma unroll 1
     while (true) {
       const uint32_t win = r.peek();
-      const uint32_t y = lds8(c5 + (win >> (32 - C15)));
-      const uint32_t b = y >> 4;
+      const uint32_t y = lds8(c5 + (win >> (32 - CW)));
+      const uint32_t b = y >> 3;
       if (y == 0 || pos + b > stop) break;
-      const uint32_t y2 = lds8(c5 + ((win << b) >> (32 - C15)));
-      const uint32_t b2 = y2 >> 4;
+      const uint32_t y2 = lds8(c5 + ((win << b) >> (32 - CW)));
+      const uint32_t b2 = y2 >> 3;
       const bool two = y2 != 0 && pos + b + b2 <= stop;
-      n += (y & 15u) + (two ? (y2 & 15u) : 0u);
+      n += (y & 7u) + (two ? (y2 & 7u) : 0u);
       const uint32_t adv = b + (two ? b2 : 0u);
       r.skip(adv);
       pos += adv;
@@ -465,10 +466,10 @@ __device__ __forceinline__ bool fdecode3(SR& r, uint32_t c, uint32_t dst, const 
 #pragma unroll (kUnroll)
     while (k2 >= 16) {
       const uint32_t win = r.peek();
-      const uint2 e = lds64(mad8(win >> (32 - FB), wl));
+      const uint2 e = lds64(mad8(win >> (32 - D3), wl));
       if (!e.y) break;
       const uint32_t b1 = (e.y >> 24) & 15u;
-      const uint2 f = lds64(mad8((win << b1) >> (32 - FB), wl));
+      const uint2 f = lds64(mad8((win << b1) >> (32 - D3), wl));
       uint32_t odd = dst & 2u, a4 = dst + odd;
       sts16(dst, e.x);
       sts32(a4, __funnelshift_r(e.x, e.y, odd << 3));
@@ -489,7 +490,7 @@ __device__ __forceinline__ bool fdecode3(SR& r, uint32_t c, uint32_t dst, const 
 #endif
 #pragma unroll (kUnroll)
     while (k2 >= 10) {
-      const uint2 e = lds64(wl + ((r.peek() >> (32 - FB)) << 3));
+      const uint2 e = lds64(wl + ((r.peek() >> (32 - D3)) << 3));
       if (!e.y) break;  // a code longer than 12 bits: one codeword below
       const uint32_t odd = dst & 2u;
       const uint32_t a4 = dst + odd;
@@ -503,7 +504,7 @@ __device__ __forceinline__ bool fdecode3(SR& r, uint32_t c, uint32_t dst, const 
     }
     if (k2 <= 0) break;
     const uint32_t win = r.peek();
-    const uint2 e = lds64(wl + ((win >> (32 - FB)) << 3));
+    const uint2 e = lds64(wl + ((win >> (32 - D3)) << 3));
     if (e.y) {
       const int32_t n = (int32_t)(e.y >> 29), k = k2 >> 1;
       const int32_t m = n < k ? n : k;
@@ -1320,15 +1321,15 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     mbar_init(bar_dt, 1);
     mbar_init(bar_off, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    mbar_expect_tx(bar_ct, T_LIMBASE + 2 * FB_SIZE + a.ljs_bytes + (MODE == M_WIDE3 ? C15_SIZE : 0) +
+    mbar_expect_tx(bar_ct, T_LIMBASE + 2 * FB_SIZE + a.ljs_bytes + (MODE == M_WIDE3 ? CW_SIZE : 0) +
                                (MODE != M_NARROW ? FB_SIZE : 0));
     if (MODE != M_NARROW) bulk_g2s(sm_s + a.t_len, tb_ + L.len12, FB_SIZE, bar_ct);
-    if (MODE == M_WIDE3) bulk_g2s(sm_s, tb_ + L.c15, C15_SIZE, bar_ct);  // decode-table region, phase 1
+    if (MODE == M_WIDE3) bulk_g2s(sm_s, tb_ + L.cwin, CW_SIZE, bar_ct);  // decode-table region, phase 1
     bulk_g2s(sm_s + a.t_c12, tb_ + L.clut12, 2 * FB_SIZE, bar_ct);
     if (a.ljs_bytes) bulk_g2s(sm_s + a.t_ljs, tb_ + L.ljsym, a.ljs_bytes, bar_ct);
     bulk_g2s(sm_s + a.t_lim, tb_ + L.lim, T_LIMBASE, bar_ct);  // lim, base (contiguous)
     if (MODE == M_WIDE3) {
-      // wlut12n replaces c15 at the phase boundary (below)
+      // wlut3 replaces cwin at the phase boundary (below)
     } else if (MODE == M_WIDE) {
       mbar_expect_tx(bar_dt, T_WIDE_DEC);
       bulk_g2s(sm_s, tb_ + L.wlut12, T_WIDE_DEC, bar_dt);
@@ -1357,7 +1358,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   T.base = sm_s + a.t_lim + 33 * 8;
   T.l12 = (MODE == M_NARROW && a.has_l12) ? sm_s + a.t_l12 : 0u;
   T.c12 = sm_s + a.t_c12;
-  T.c15 = MODE == M_WIDE3 ? sm_s : 0u;
+  T.cw = MODE == M_WIDE3 ? sm_s : 0u;
   T.len12 = sm_s + a.t_len;
   T.ljs = (a.ljs_bytes && hdr->kind == 0) ? sm_s + a.t_ljs : 0u;
   T.t = table_view(a.table, a.max_codes, hdr->ncodes);
@@ -1563,13 +1564,13 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       sts128(sm_s + 16 * i, lds128(sm_s + a.t_wp + 16 * (i >> 3)));
   __syncthreads();  // tile totals and the replicated decode table visible
   if (MODE == M_WIDE3 && threadIdx.x == 0) {
-    // every warp is done with c15: the decode table takes its place
+    // every warp is done with cwin: the decode table takes its place
     TableLayout L(a.max_codes);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     mbar_expect_tx(bar_dt, T_WIDE3_DEC);
-    bulk_g2s(sm_s, static_cast<const char*>(a.table) + L.wlut12n, T_WIDE3_DEC, bar_dt);
+    bulk_g2s(sm_s, static_cast<const char*>(a.table) + L.wlut3, T_WIDE3_DEC, bar_dt);
   }
-  T.c15 = 0u;
+  T.cw = 0u;
   if (threadIdx.x == 0) {
     atomicMax(&a.rep->phase_ns[VAR == BH_VARIANT_GAP ? 2 : 1], s_tcount);
     if (VAR == BH_VARIANT_SYNC) atomicMax(&a.rep->phase_ns[2], s_tseam);
@@ -1651,7 +1652,11 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   unsigned long long Pc = 0;
   auto grab = [&]() -> uint64_t {
     uint32_t v = 0;
-    if (lane == 0) v = atomicAdd(&s_next, 1u);
+    // one lane's shared-memory increment (an add would be wrapped in the
+    // compiler's warp-aggregation sequence; inc with a limit that is never
+    // reached is the same add)
+    if (lane == 0)
+      asm volatile("atom.shared.inc.u32 %0, [%1], 0xfffffffe;" : "=r"(v) : "r"(smem_u32(&s_next)) : "memory");
     return pick(__shfl_sync(0xffffffffu, v, 0));
   };
   // the tile's lane info (entry, prefix) and seam delta are loaded one tile
@@ -1663,7 +1668,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
     if (VAR == BH_VARIANT_SYNC) dlt_n = a.tile_dlt[tile];
   }
   uint32_t dk = 0;  // tiles decoded (trace slots)
-  if (MODE == M_WIDE3) mbar_wait(bar_dt, 0);  // the decode table has replaced c15
+  if (MODE == M_WIDE3) mbar_wait(bar_dt, 0);  // the decode table has replaced cwin
   for (; tile < t1;) {
     const uint64_t tn = grab();
     const uint32_t info = info_n;
@@ -1856,7 +1861,33 @@ struct FusedCfg {
       t_len;
 };
 
-FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
+// Dynamic shared memory one CTA of the variant's kernel may use on the
+// current device: the per-block opt-in limit minus the kernel's static
+// arrays (the self-sync kernel keeps its seam descriptors there), cached per
+// (device, variant); 219 KB without a device.
+uint32_t smem_budget(int variant) {
+  static std::atomic<uint32_t> cache[64][2];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 219u * 1024u;
+  const int vi = variant == BH_VARIANT_SYNC ? 1 : 0;
+  uint32_t b = cache[dev][vi].load(std::memory_order_relaxed);
+  if (!b) {
+    int optin = 0;
+    cudaFuncAttributes fa;
+    const void* fn = vi ? (const void*)k_fused2<BH_VARIANT_SYNC, 0, M_NARROW>
+                        : (const void*)k_fused2<BH_VARIANT_GAP, 0, M_NARROW>;
+    if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess ||
+        cudaFuncGetAttributes(&fa, fn) != cudaSuccess || optin <= (int)fa.sharedSizeBytes) {
+      cudaGetLastError();
+      return 219u * 1024u;
+    }
+    b = (uint32_t)(optin - (int)fa.sharedSizeBytes);
+    cache[dev][vi].store(b, std::memory_order_relaxed);
+  }
+  return b;
+}
+
+FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr, int variant = BH_VARIANT_SYNC) {
   FusedCfg c;
   const uint32_t seq_bits = vsb_of(s) * TILE_SUBSEQ;
   // words one tile can stage: its span (+1 for a straddle), the 16-byte
@@ -1906,8 +1937,8 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr) {
   // two word buffers, staging
   c.per_warp = (uint32_t)align16(8 * (size_t)c.wpb + 2 * (size_t)c.cap + 32);
   // dynamic shared memory budget: 227 KB per CTA minus the kernel's static
-  // arrays (tile totals, seam descriptors: < 8 KB)
-  const int fit = (int)(((int64_t)(219 * 1024) - (int64_t)c.tables) / (int64_t)c.per_warp);
+  // arrays (tile totals; the self-sync kernel's seam descriptors)
+  const int fit = (int)(((int64_t)smem_budget(variant) - (int64_t)c.tables) / (int64_t)c.per_warp);
   int w = env_int("BH_FUSED_WARPS", 0);
   if (w <= 0 || w > fit) w = fit;
   if (w > FUSED_MAX_WARPS) w = FUSED_MAX_WARPS;
@@ -1954,8 +1985,8 @@ extern "C" int bh_fused_supported(const bh_stream* s, int variant) {
   const uint64_t seq_bits = (uint64_t)vsb_of(s) * TILE_SUBSEQ;
   if (seq_bits > 16384 || s->total_bits >= (1ull << 36) || s->symbol_count >= (1ull << 36)) return 0;
   if (variant == BH_VARIANT_GAP && !s->gap_dev) return 0;
-  FusedCfg c = fused_cfg(s);
-  return c.smem <= 219 * 1024 ? 1 : 0;
+  FusedCfg c = fused_cfg(s, nullptr, variant);
+  return c.smem <= smem_budget(variant) ? 1 : 0;
 }
 
 // workspace: [64 B header: epoch, CTA-done counter][cnt desc][exit desc]
@@ -2003,7 +2034,7 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   (void)tune;
   const uint64_t nseq = nseq_of(s);
   if (ws_bytes < bh_fused_workspace_bytes(s, variant, tune)) return BH_BAD_ARGUMENT;
-  FusedCfg cfg = fused_cfg(s, tune);
+  FusedCfg cfg = fused_cfg(s, tune, variant);
   FusedArgs a;
   a.words = s->words_dev;
   a.words_alloc = (((s->total_bits + 31) / 32 + BH_WORD_PAD) & ~3ull);

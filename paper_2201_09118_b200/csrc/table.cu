@@ -172,7 +172,7 @@ __global__ void k_explicit_hdr(const uint8_t* __restrict__ lens, uint32_t alphab
   }
 }
 
-// 8-byte entry of up to three whole codewords of the 12-bit window v (wlut12n)
+// 8-byte entry of up to three whole codewords (wlut3)
 __device__ __forceinline__ uint2 pack3(uint32_t s0, uint32_t s1, uint32_t s2, uint32_t n3, uint32_t l0, uint32_t p3) {
   uint2 e;
   e.x = s0 | (s1 << 16);
@@ -180,17 +180,21 @@ __device__ __forceinline__ uint2 pack3(uint32_t s0, uint32_t s1, uint32_t s2, ui
   return e;
 }
 
-__device__ __forceinline__ uint2 narrow3(uint32_t a, uint32_t b, uint32_t c, int v, const uint32_t* s_l12) {
-  uint32_t p = 0, n = 0, l0 = 0;
-  while (n < 3 && p < (uint32_t)FB) {
-    const uint32_t f = s_l12[((uint32_t)v << p) & (FB_SIZE - 1)];
-    const uint32_t len = (f >> 16) & 0xff;
-    if (len == 0 || p + len > (uint32_t)FB) break;
+// wlut3 entry of the D3-bit window v: up to three whole codewords, each read
+// from the 12-bit prefix table at its offset (the next 12 bits, zero-filled
+// past the window: a codeword that fits inside the window matches the same)
+__device__ __forceinline__ uint2 wlut3_entry(uint32_t v, const uint32_t* s_l12) {
+  uint32_t p = 0, n = 0, l0 = 0, sy[3] = {0, 0, 0};
+#pragma unroll 1
+  while (n < 3 && p < (uint32_t)D3) {
+    const uint32_t f = s_l12[((v << p) >> (D3 - FB)) & (FB_SIZE - 1)];
+    const uint32_t len = (f >> 16) & 0xffu;
+    if (len == 0 || p + len > (uint32_t)D3) break;
     if (n == 0) l0 = len;
+    sy[n++] = f & 0xffffu;
     p += len;
-    ++n;
   }
-  return pack3(n > 0 ? a : 0u, n > 1 ? b : 0u, n > 2 ? c : 0u, n, l0, p);
+  return pack3(sy[0], sy[1], sy[2], n, l0, p);
 }
 
 // First-level tables from the sorted long-code arrays (one CTA).
@@ -238,7 +242,6 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
   __syncthreads();
   // up to six whole codewords of the 12-bit window (wide decode table)
   uint4* wlut12 = reinterpret_cast<uint4*>(reinterpret_cast<char*>(blob) + L.wlut12);
-  uint2* wlut12n = reinterpret_cast<uint2*>(reinterpret_cast<char*>(blob) + L.wlut12n);
   for (int v = threadIdx.x; v < FB_SIZE; v += blockDim.x) {
     uint32_t p6 = 0, n6 = 0, sy[6] = {0, 0, 0, 0, 0, 0}, l0 = 0;
     while (n6 < 6 && p6 < (uint32_t)FB) {
@@ -255,26 +258,27 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
     wl.z = sy[4] | (sy[5] << 16);
     wl.w = n6 ? (p6 | (n6 << 4) | (l0 << 16) | ((2 * n6) << 28)) : 0u;
     wlut12[v] = wl;
-    wlut12n[v] = narrow3(sy[0], sy[1], sy[2], v, s_l12);
   }
-  uint8_t* c15 = reinterpret_cast<uint8_t*>(reinterpret_cast<char*>(blob) + L.c15);
+  uint2* wlut3 = reinterpret_cast<uint2*>(reinterpret_cast<char*>(blob) + L.wlut3);
+  for (uint32_t v = threadIdx.x; v < (uint32_t)D3_SIZE; v += blockDim.x) wlut3[v] = wlut3_entry(v, s_l12);
+  uint8_t* cwin = reinterpret_cast<uint8_t*>(reinterpret_cast<char*>(blob) + L.cwin);
   __shared__ uint32_t s_minl;
   if (threadIdx.x == 0) s_minl = 64;
   __syncthreads();
   for (uint32_t i = threadIdx.x; i < t.ncodes; i += blockDim.x) atomicMin(&s_minl, (uint32_t)t.ljlen[i]);
   __syncthreads();
-  const bool build15 = s_minl >= 4 && s_minl != 64;
-  for (int v = threadIdx.x; v < C15_SIZE; v += blockDim.x) {
-    const uint32_t w0 = (uint32_t)v << (32 - C15);
+  const bool buildcw = s_minl >= 4 && s_minl != 64;
+  for (int v = threadIdx.x; v < CW_SIZE; v += blockDim.x) {
+    const uint32_t w0 = (uint32_t)v << (32 - CW);
     uint32_t pos = 0, n = 0;
-    while (build15 && pos < (uint32_t)C15) {
+    while (buildcw && pos < (uint32_t)CW) {
       uint32_t len = (s_l12[(w0 << pos) >> (32 - FB)] >> 16) & 0xffu;
       if (!len) len = (slow_lookup(t, w0 << pos) >> 16) & 0xffu;
-      if (len == 0 || pos + len > (uint32_t)C15) break;
+      if (len == 0 || pos + len > (uint32_t)CW) break;
       pos += len;
       ++n;
     }
-    c15[v] = (uint8_t)(n | (pos << 4));
+    cwin[v] = (uint8_t)(n | (pos << 3));
   }
   uint16_t* s_len12 = reinterpret_cast<uint16_t*>(s_lut);  // 4096 lengths (8 KB)
   for (int v = threadIdx.x; v < FB_SIZE; v += blockDim.x) s_len12[v] = (uint16_t)((s_l12[v] >> 16) & 0xff);
@@ -522,7 +526,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   }
   __syncthreads();
   K1ST(4);
-  // direct tables: 12-bit (lut12, clut12, wlut12, wlut12n), 11-bit (lut, cnt)
+  // direct tables: 12-bit (lut12, clut12, wlut12), 11-bit (lut, cnt)
   // and 8-bit (dlut8, clut8, wlut8) entries spread over every thread of the
   // grid.  A codeword at offset pos of a W-bit window v is S.l12 of the 12
   // bits (v << (12 - W + pos)), zero-filled: it lies inside the window when
@@ -542,28 +546,31 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   // fused kernel counts with it -- and all zero, "use the 12-bit table",
   // otherwise)
   K1ST(5);
-  uint8_t* c15 = reinterpret_cast<uint8_t*>(B + L.c15);
-  const bool build15 = S.minl >= 4;
-  for (uint32_t v = cta * K1_THREADS + tid; v < (uint32_t)C15_SIZE; v += G * K1_THREADS) {
-    const uint32_t w0 = v << (32 - C15);
+  uint8_t* cwin = reinterpret_cast<uint8_t*>(B + L.cwin);
+  const bool buildcw = S.minl >= 4;
+  for (uint32_t v = cta * K1_THREADS + tid; v < (uint32_t)CW_SIZE; v += G * K1_THREADS) {
+    const uint32_t w0 = v << (32 - CW);
     uint32_t pos = 0, n = 0;
-    while (build15 && pos < (uint32_t)C15) {
+    while (buildcw && pos < (uint32_t)CW) {
       uint32_t len = (S.l12[(w0 << pos) >> (32 - FB)] >> 16) & 0xffu;
       if (!len) len = (canon_one(S, w0 << pos) >> 16) & 0xffu;  // > 12 bits (or no codeword)
-      if (len == 0 || pos + len > (uint32_t)C15) break;
+      if (len == 0 || pos + len > (uint32_t)CW) break;
       pos += len;
       ++n;
     }
-    c15[v] = (uint8_t)(n | (pos << 4));
+    cwin[v] = (uint8_t)(n | (pos << 3));
   }
+  uint2* wlut3 = reinterpret_cast<uint2*>(B + L.wlut3);
+  for (uint32_t v = cta * K1_THREADS + tid; v < (uint32_t)D3_SIZE; v += G * K1_THREADS)
+    wlut3[v] = wlut3_entry(v, S.l12);
   for (uint32_t it = cta * K1_THREADS + tid; it < N12 + N11 + N8; it += G * K1_THREADS) {
     const uint32_t W = it < N12 ? (uint32_t)FB : it < N12 + N11 ? (uint32_t)LUT_BITS : 8u;
     const uint32_t v = it < N12 ? it : it < N12 + N11 ? it - N12 : it - N12 - N11;
     const uint32_t v12 = v << (FB - W);
     const uint32_t e0 = S.l12[v12];
     // every whole codeword of the window: start mask, end, count; the first
-    // six (three) also for the multi-symbol decode tables
-    uint32_t pos = 0, starts = 0, n = 0, n6 = 0, l0 = 0, p6 = 0, p3 = 0, sx = 0, sy = 0, sz = 0;
+    // six also for the multi-symbol decode tables
+    uint32_t pos = 0, starts = 0, n = 0, n6 = 0, l0 = 0, p6 = 0, sx = 0, sy = 0, sz = 0;
     while (pos < W) {
       const uint32_t e = pos ? S.l12[(v12 << pos) & (FB_SIZE - 1)] : e0;
       const uint32_t len = (e >> 16) & 0xffu;
@@ -573,7 +580,6 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
         if (n6 == 0) l0 = len;
         pack6(sx, sy, sz, n6++, e & 0xffffu);
         p6 = pos + len;
-        if (n6 <= 3) p3 = p6;
       }
       pos += len;
       ++n;
@@ -589,9 +595,6 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
       clut12[v] = (uint16_t)(starts | (pos << 12));
       wl.w = n6 ? (p6 | (n6 << 4) | (l0 << 16) | ((2 * n6) << 28)) : 0u;
       wlut12[v] = wl;
-      const uint32_t n3 = n6 < 3 ? n6 : 3;
-      reinterpret_cast<uint2*>(B + L.wlut12n)[v] =
-          pack3(sx & 0xffffu, n3 > 1 ? sx >> 16 : 0u, n3 > 2 ? sy & 0xffffu : 0u, n3, l0, p3);
     } else if (it < N12 + N11) {
       lut[v] = first;
       cnt[v] = n ? (uint16_t)(pos | (n << 8)) : (uint16_t)0;

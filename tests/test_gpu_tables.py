@@ -31,9 +31,9 @@ def layout(max_codes: int) -> dict:
     L["lut12"] = a16(L["wlut8"] + 16 * 256)
     L["clut12"] = L["lut12"] + 4 * 4096
     L["wlut12"] = a16(L["clut12"] + 2 * 4096)
-    L["wlut12n"] = a16(L["wlut12"] + 16 * 4096)
-    L["c15"] = a16(L["wlut12n"] + 8 * 4096)
-    L["len12"] = a16(L["c15"] + 32768)
+    L["wlut3"] = a16(L["wlut12"] + 16 * 4096)
+    L["cwin"] = a16(L["wlut3"] + 8 * 8192)
+    L["len12"] = a16(L["cwin"] + 65536)
     L["lim"] = a16(L["len12"] + 4096)
     L["base"] = L["lim"] + 8 * 33
     L["lj"] = a16(L["base"] + 8 * 33)
@@ -87,11 +87,11 @@ def test_canonical_tables_match_general_builder(env):
         assert np.array_equal(hf[1:7], hg[1:7]), (hf[:7], hg[:7])  # max_len ncodes lut_bits alphabet status complete
         ncodes = int(hf[2])
         assert ncodes == len(book.entries)
-        for name in ("lut", "cnt", "dlut8", "clut8", "wlut8", "lut12", "clut12", "wlut12", "wlut12n", "c15",
+        for name in ("lut", "cnt", "dlut8", "clut8", "wlut8", "lut12", "clut12", "wlut12", "wlut3", "cwin",
                      "len12"):
             nxt = {"lut": "cnt", "cnt": "dlut8", "dlut8": "clut8", "clut8": "wlut8", "wlut8": "lut12",
-                   "lut12": "clut12", "clut12": "wlut12", "wlut12": "wlut12n", "wlut12n": "c15",
-                   "c15": "len12", "len12": "lim"}[name]
+                   "lut12": "clut12", "clut12": "wlut12", "wlut12": "wlut3", "wlut3": "cwin",
+                   "cwin": "len12", "len12": "lim"}[name]
             assert np.array_equal(f[L[name]:L[nxt]], g[L[name]:L[nxt]]), (name, book.max_len, ncodes)
         for name, w in (("lj", 4), ("ljsym", 2), ("ljlen", 1)):
             assert np.array_equal(f[L[name]:L[name] + w * ncodes], g[L[name]:L[name] + w * ncodes]), name
@@ -104,11 +104,31 @@ def test_canonical_tables_match_general_builder(env):
             code = (code + int(counts[ln])) << 1
 
 
-def test_count15_table_semantics(env):
-    """c15 (15-bit count table of the long-code path): for a book with every
-    code >= 4 bits, entry v = (whole codewords of the zero-filled 15-bit
-    window v) | (their end) << 4, checked against a host walk of the
-    canonical codes; all zero for books with shorter codes."""
+def _host_lengths(book):
+    """codeword length at the front of a 32-bit window (0: none), by the
+    canonical codes"""
+    import bisect
+    left = sorted(((code << (32 - ln)), ln, sym) for sym, (code, ln) in book.entries.items())
+    keys = [k for k, _, _ in left]
+
+    def at(w):
+        i = bisect.bisect_right(keys, w) - 1
+        if i < 0:
+            return 0, 0
+        k, ln, sym = left[i]
+        return (ln, sym) if (w ^ k) >> (32 - ln) == 0 else (0, 0)
+    return at
+
+
+def test_count_and_three_codeword_table_semantics(env):
+    """cwin (16-bit count table of the long-code path): for a book with every
+    code >= 4 bits, entry v = (whole codewords of the zero-filled 16-bit
+    window v) | (their end) << 3; all zero for books with shorter codes.
+    wlut3 (13-bit three-codeword decode table): up to three whole codewords
+    of 12 bits or less inside the 13-bit window, x = s0 | s1 << 16,
+    y = s2 | len0 << 16 | end << 24 | 2n << 28 (0 when the first code is
+    longer than 12 bits or ends past the window).  Both against a host walk
+    of the canonical codes."""
     torch, ph, _lib = env
     lib = _lib.load()
     st = torch.cuda.current_stream().cuda_stream
@@ -122,28 +142,36 @@ def test_count15_table_semantics(env):
         lens = book.length_bytes()
         tab = torch.zeros(L["total"], dtype=torch.uint8, device="cuda")
         _lib.check(lib.bh_table_build(torch.from_numpy(lens.copy()).cuda().data_ptr(), len(lens), tab.data_ptr(), mc, st))
-        c15 = tab[L["c15"]:L["c15"] + 32768].cpu().numpy()
+        t = tab.cpu().numpy()
+        cwin = t[L["cwin"]:L["cwin"] + 65536]
+        at = _host_lengths(book)
         if not want_built:
-            assert not c15.any()
-            continue
-        # host: left-justified code -> length, by the canonical limits
-        left = sorted(((code << (32 - ln)), ln) for code, ln in book.entries.values())
-        import bisect
-        keys = [k for k, _ in left]
-
-        def length_at(w):  # codeword length at the front of 32-bit window w (0: none)
-            i = bisect.bisect_right(keys, w) - 1
-            if i < 0:
-                return 0
-            k, ln = left[i]
-            return ln if (w ^ k) >> (32 - ln) == 0 else 0
-        for v in list(range(0, 32768, 97)) + [0, 32767, 12345]:
-            w0 = v << 17
-            pos = n = 0
-            while pos < 15:
-                ln = length_at((w0 << pos) & 0xffffffff)
-                if ln == 0 or pos + ln > 15:
-                    break
-                pos += ln
-                n += 1
-            assert c15[v] == (n | (pos << 4)), (sigma, v, c15[v], n, pos)
+            assert not cwin.any()
+        else:
+            for v in list(range(0, 65536, 193)) + [0, 65535, 12345]:
+                w0 = v << 16
+                pos = n = 0
+                while pos < 16:
+                    ln, _ = at((w0 << pos) & 0xffffffff)
+                    if ln == 0 or pos + ln > 16:
+                        break
+                    pos += ln
+                    n += 1
+                assert cwin[v] == (n | (pos << 3)), (sigma, v, cwin[v], n, pos)
+            w3 = t[L["wlut3"]:L["wlut3"] + 8 * 8192].view(np.uint32).reshape(-1, 2)
+            for v in list(range(0, 8192, 37)) + [0, 8191]:
+                w0 = v << 19
+                pos = n = l0 = 0
+                syms = []
+                while n < 3 and pos < 13:
+                    ln, sym = at((w0 << pos) & 0xffffffff)
+                    if ln == 0 or ln > 12 or pos + ln > 13:
+                        break
+                    l0 = l0 or ln
+                    syms.append(sym)
+                    pos += ln
+                    n += 1
+                syms += [0] * (3 - len(syms))
+                want_x = syms[0] | (syms[1] << 16)
+                want_y = (syms[2] | (l0 << 16) | (pos << 24) | ((2 * n) << 28)) if n else 0
+                assert (int(w3[v, 0]), int(w3[v, 1])) == (want_x, want_y), (sigma, v)

@@ -14,7 +14,7 @@ from bench import load_synth  # noqa: E402
 
 synth = load_synth()
 lib = _lib.load()
-names = ["launch->hist", "hist", "scan", "ranks", "l12", "(c15 start)", "c15+fill"]
+names = ["launch->hist", "hist", "scan", "ranks", "l12", "(cwin start)", "cwin+wlut3+fill"]
 for name in ("hurricane", "hacc", "nyx4096"):
     codes = synth.field_codes(synth.FIELDS[name], n=2_000_000)
     book = ph.book_for(codes, 16)
