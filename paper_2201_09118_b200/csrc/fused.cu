@@ -104,6 +104,10 @@ struct FusedArgs {
   DevReport* rep;
   unsigned int* ws_hdr;  // [0] epoch of the last completed call, [1] CTAs done
   uint32_t wpb;          // words per tile buffer (multiple of 4)
+  uint32_t halo;         // words staged past a tile's span (SYNC: the next tile's first slot, for its seam walk)
+  uint32_t lead;         // words staged before a tile's span (SYNC: the pre-synchronisation of its first slot)
+  uint32_t presync;      // SYNC: bits a lane's count parse starts before its boundary (0: at the boundary; <= 32 lead)
+  uint32_t walk_max;     // SYNC: seam-walk window past the next boundary (test knob; ~0 = the staged words)
   uint32_t cap;          // staging symbols per warp (multiple of 8)
   uint32_t warps;        // warps per CTA
   uint32_t per_warp_bytes;
@@ -635,6 +639,71 @@ __device__ __forceinline__ bool resync_step(uint32_t base_s, uint32_t eo, uint32
   }
 }
 
+// Overlap pre-synchronisation (self-sync count phase): the first codeword
+// start at or after boundary b of the parse entered at p < b, walked a whole
+// 12-bit count-table entry at a time (start mask + end).  A parse entered K
+// bits early has almost always synchronised with the true one by b, so the
+// result is the lane's true entry far more often than b itself: the intra-
+// sequence rounds then find the predecessor's exit equal to it and skip the
+// re-decode.  Any result is correct (the rounds re-synchronise a wrong one).
+template <int MODE>
+__device__ __forceinline__ uint32_t presync(uint32_t base_s, uint32_t p, uint32_t b, const FTab& T) {
+  SR r;
+  r.init(base_s, p);
+  const uint32_t ct = T.c12;
+#pragma unroll 1
+  while (true) {
+    const uint32_t win = r.peek();
+    const uint32_t y = lds16(ct + ((win >> (32 - FB)) << 1));
+    if (!y) {  // a code longer than 12 bits
+      const uint32_t l = (fslow(win, T.lim, T.base, T.t.ljsym, T.kind, T.t, T.ljs) >> 16) & 0xffu;
+      if (!l) return b;
+      p += l;
+      if (p >= b) return p;
+      r.skip(l);
+      continue;
+    }
+    const uint32_t mask = y & 0xfffu, end = y >> 12, d = b - p;
+    if (d < end) {
+      const uint32_t hi = mask >> d;
+      return hi ? b + __ffs(hi) - 1 : p + end;
+    }
+    p += end;
+    if (p == b) return b;
+    r.skip(end);
+  }
+}
+
+// Seam walk (self-sync, a seam inside the CTA's range): the parse entered at
+// the true seed en against the first slot's own parse from eo, codeword by
+// codeword, until they meet (sync_decoder.py:90-101).  delta = seed-parse
+// codewords minus own-parse codewords before the meeting point, so the slot's
+// count for the seed is its own count + delta and its exit is unchanged.
+// False when they do not meet below `stop` (the slot's exit may change) or
+// below `lim` (the end of the staged words).
+template <int MODE>
+__device__ __forceinline__ bool seam_walk(uint32_t base_s, uint32_t eo, uint32_t en, uint32_t stop, uint32_t lim,
+                                          const FTab& T, int32_t& delta) {
+  delta = 0;
+  uint32_t po = eo, pn = en;
+  if (po == pn) return true;
+  int32_t d = 0;
+  SR ro, rn;
+  ro.init(base_s, po);
+  rn.init(base_s, pn);
+  while (po != pn) {
+    const bool adv_o = po < pn;
+    const uint32_t lo = adv_o ? po : pn;
+    if (lo >= stop || lo >= lim) return false;
+    const uint32_t l = clen<MODE>(adv_o ? ro.peek() : rn.peek(), T);
+    if (!l) return false;
+    if (adv_o) { ro.skip(l); po += l; --d; }
+    else { rn.skip(l); pn += l; ++d; }
+  }
+  delta = d;
+  return true;
+}
+
 template <int MODE>
 __device__ __forceinline__ bool resync(uint32_t base_s, uint32_t eo, uint32_t co, uint32_t xo, uint32_t en,
                                        uint32_t stop, const FTab& T, uint32_t& cn, uint32_t& xn) {
@@ -782,8 +851,9 @@ __device__ __forceinline__ void wstage_init(WStage& ws, uint32_t bar) {
 __device__ __forceinline__ uint64_t stage_words(const FusedArgs& a, uint64_t tile, uint32_t land_s, uint32_t& nch,
                                                 WStage& ws, bool last_use = false) {
   const uint64_t s0 = tile * (uint64_t)a.seq_bits;
-  const uint64_t w0 = (s0 >> 5) & ~3ull;
-  uint64_t w1 = ((s0 + a.seq_bits) >> 5) + HALO_WORDS;
+  uint64_t w0 = (s0 >> 5) & ~3ull;
+  w0 = w0 >= a.lead ? w0 - a.lead : 0;
+  uint64_t w1 = ((s0 + a.seq_bits) >> 5) + a.halo;
   w1 = (w1 + 3) & ~3ull;
   if (w1 > a.words_alloc) w1 = a.words_alloc;
   nch = (uint32_t)((w1 - w0) >> 2);
@@ -1019,7 +1089,8 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
                                             uint64_t wb0, uint32_t nsl, uint32_t ep, uint32_t& e, uint32_t& c,
                                             bool& bad, int32_t seed_o = -1, uint32_t* cand_out = nullptr,
                                             bool* fullfix = nullptr, const uint32_t* gpre = nullptr,
-                                            unsigned long long* desc_out = nullptr) {
+                                            unsigned long long* desc_out = nullptr, bool chase = true,
+                                            uint32_t* xlast_out = nullptr) {
   bool resync_needed = false;  // GAP, spl > 1: an inner gap entry is not a codeword start
   const uint32_t lane = threadIdx.x & 31;
   const uint32_t sb = a.sb;
@@ -1063,6 +1134,10 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
   } else {
     stop = min(b + sb, tbr);
     if (tile == 0 && lane == 0) e = x = b + a.first_entry;  // chunk of a longer stream
+    // entry guess: pre-synchronised from BH_PRESYNC bits before the boundary,
+    // except for a first slot resolved by candidate seeds (they count from b)
+    else if (a.presync && active && (lane > 0 || !chase))
+      e = x = presync<MODE>(base_s, b > a.presync ? b - a.presync : 0u, b, T);
     if (active && e < stop) {
       SR r;
       r.init(base_s, e);
@@ -1094,7 +1169,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
     const uint32_t x0 = __shfl_sync(0xffffffffu, x, 0);
     uint32_t cand_c = c0, cand_x = x0;
     bool indep = true;
-    if (tile > 0) {
+    if (tile > 0 && chase) {
       // the true seed lies within the codeword straddling the boundary, so
       // only offsets below the longest code length are candidates
 #ifndef BH_X_NOCAND
@@ -1109,6 +1184,7 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
       indep = __all_sync(0xffffffffu, cand_x == x0);
     }
     const uint32_t xlast = __shfl_sync(0xffffffffu, x, nsl - 1);
+    if (xlast_out) *xlast_out = xlast;
     if (seed_o < 0 && !indep) {
       // The candidates disagree after the first slot: follow the candidate
       // set through the next slots (lane j carries seed j) until it collapses
@@ -1132,7 +1208,9 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
     if (seed_o < 0) {
       // speculative: publish the exit when it does not depend on the seed
       if (cand_out) *cand_out = cand_c;
-      const unsigned long long dsc = mkdesc(ep, indep ? D_INC : D_AGG, indep ? wb0 + xlast : 0);
+      // without the candidate chase (a seam inside the range, resolved by the
+      // seam walk) the exit is speculative: D_AGG carrying its value
+      const unsigned long long dsc = mkdesc(ep, indep && chase ? D_INC : D_AGG, indep ? wb0 + xlast : 0);
       if (lane == 0) st_relaxed(a.exit_desc + tile, dsc);
       if (desc_out) *desc_out = dsc;
     } else if (tile > 0) {
@@ -1261,6 +1339,11 @@ __device__ unsigned long long lookback_wide(unsigned long long* desc, uint64_t c
 }
 
 constexpr uint32_t MAX_SMEM_TILES = 512;
+#ifndef BH_SEAMWALK
+#define BH_SEAMWALK 1  // SYNC: in-range seams by one walk from the predecessor's exit (0: 32 candidate seeds per tile)
+#endif
+constexpr uint32_t SEAM_FAIL = 0xffffffffu;
+constexpr uint32_t FAIL_CAP = 128;  // seam-walk failures listed per CTA (more: an ordered scan)
 constexpr int32_t FULL_FIX = 0x7fffffff;  // tile_dlt marker: re-synchronise the whole tile in the fix-up
 
 template <int VAR, int TR, int MODE>
@@ -1287,6 +1370,8 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   __shared__ uint32_t s_cls[TUNE_CLASSES];           // tuner: sequences per class
   __shared__ __align__(8) unsigned long long s_wbar[FUSED_MAX_WARPS];  // per-warp word-staging mbarriers
   __shared__ uint32_t s_tcnt[MAX_SMEM_TILES];  // symbols per tile of the range (short ranges)
+  __shared__ uint32_t s_fail[BH_SEAMWALK && VAR == BH_VARIANT_SYNC ? FAIL_CAP : 1];  // seam-walk failures (tile - t0)
+  __shared__ uint32_t s_nfail;
   // SYNC, short ranges: the range's exit descriptors and full-fix flags, so
   // the seam fix-up reads in-range predecessors from shared memory
   constexpr uint32_t SX = VAR == BH_VARIANT_SYNC ? MAX_SMEM_TILES : 1;
@@ -1404,20 +1489,45 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
       if (VAR == BH_VARIANT_GAP) gap_load(tn, gnext);
     }
     const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - tile * a.sps);
-    uint32_t e, c, cand = 0;
+    uint32_t e, c, cand = 0, xl = 0;
     bool fullfix = false;
     unsigned long long dsc = 0;
+    // SYNC: only the range's first tile resolves its seam by candidate seeds
+    // (its predecessor belongs to another CTA); the other seams are walked
+    // from the predecessor's exit below
+    const bool chase = !BH_SEAMWALK || tile == t0;
     tile_counts<VAR, MODE>(a, T, tile, dbuf_s, wb_a, nsl, ep, e, c, bad, -1, &cand, &fullfix,
-                     VAR == BH_VARIANT_GAP && a.sps == 32 ? gcur : nullptr, &dsc);
+                     VAR == BH_VARIANT_GAP && a.sps == 32 ? gcur : nullptr, &dsc, chase, &xl);
     if (kidx < 8) MARK(11 + 2 * kidx);
     gcur[0] = gnext[0];
     gcur[1] = gnext[1];
     if (VAR == BH_VARIANT_SYNC) {
-      if (scand) sts16(stg_s + 64 * kidx + 2 * lane, min(cand, 0xffffu));
-      else a.cand[tile * 32 + lane] = (uint16_t)min(cand, 0xffffu);
+      if (chase) {
+        if (scand) sts16(stg_s + 64 * kidx + 2 * lane, min(cand, 0xffffu));
+        else a.cand[tile * 32 + lane] = (uint16_t)min(cand, 0xffffu);
+      }
       if (lane == 0) {
         a.tile_dlt[tile] = fullfix ? FULL_FIX : 0;
         if (srange) *(volatile unsigned long long*)&s_texit[tile - t0] = dsc;
+#if BH_SEAMWALK
+        // the next tile's seam: its first slot's parse from this tile's
+        // (speculative) exit against its boundary parse, over the halo words
+        // staged with this tile.  Seam word: seed | (delta + 0x8000) << 16,
+        // SEAM_FAIL when the parses do not meet (the serial pass takes it)
+        if (tile + 1 < t1) {
+          const uint32_t bn = (uint32_t)((tile + 1) * a.seq_bits - wb_a);
+          const uint32_t tbr = (uint32_t)min(a.tb - wb_a, (uint64_t)0xffffffffu);
+          const uint32_t o = xl - bn;
+          // the next tile's first slot parses from its pre-synchronised entry
+          const uint32_t en = a.presync ? presync<MODE>(dbuf_s, bn > a.presync ? bn - a.presync : 0u, bn, T) : bn;
+          int32_t d;
+          uint32_t sw = SEAM_FAIL;
+          const uint32_t lim = min(32 * (4 * nch_a - 4), bn + min(a.walk_max, a.sb));
+          if (o < 32 && seam_walk<MODE>(dbuf_s, en, xl, min(bn + a.sb, tbr), lim, T, d))
+            sw = o | ((uint32_t)(d + 0x8000) << 16);
+          *reinterpret_cast<uint32_t*>(a.cand + (tile + 1) * 32) = sw;
+        }
+#endif
       }
     }
     ++kidx;
@@ -1442,6 +1552,152 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
   if (lane == 0) atomicMax(&s_tcount, global_ns());
   MARK(9);
   if (VAR == BH_VARIANT_SYNC) {
+#if BH_SEAMWALK
+    // Seam fix-up (inter_sync, sync_decoder.py:116-149).  Every seam inside
+    // the range was walked in the count loop from the predecessor's
+    // speculative exit.  Where the walk met the boundary parse, the first
+    // slot's count changes by its delta and the tile's exit is unchanged, so
+    // -- by induction from the range's first tile, whose exit the candidate
+    // seeds proved seed-independent -- every speculative exit is final.  The
+    // rest (walks that did not meet, a first tile whose exit depends on its
+    // seed, successors of a tile whose exit changed) warp 0 finishes in tile
+    // order, re-synchronising each from its known seed.
+    if (threadIdx.x == 0) s_nfail = 0;
+    __syncthreads();  // seam words, speculative exits and counts of every warp visible
+    for (uint64_t t = t0 + 1 + threadIdx.x; t < t1; t += blockDim.x) {
+      const uint32_t sw = *reinterpret_cast<const uint32_t*>(a.cand + t * 32);
+      if (sw == SEAM_FAIL) {
+        const uint32_t k = atomicAdd(&s_nfail, 1u);
+        if (k < FAIL_CAP) s_fail[k] = (uint32_t)(t - t0);
+        continue;
+      }
+      const uint32_t o = sw & 0xffffu;
+      const int32_t d = (int32_t)(sw >> 16) - 0x8000;
+      a.tile_dlt[t] = d;
+      a.lane_info[t * 32] = o;  // first slot enters at the seed; prefix 0
+      if (srange) s_tcnt[t - t0] += (uint32_t)d;
+      else a.tile_cnt[t] += (uint32_t)d;
+    }
+    __syncthreads();
+    if (wib == 0 && t0 < t1) {
+      const uint32_t nfail = s_nfail;
+      auto exit_of = [&](uint64_t t) -> unsigned long long {
+        return srange ? *(volatile unsigned long long*)&s_texit[t - t0] : ld_relaxed(a.exit_desc + t);
+      };
+      // seed offset of tile t from its predecessor's final exit (another CTA's)
+      auto pred_seed = [&](uint64_t t) -> uint32_t {
+        unsigned long long dp = 0;
+        if (lane == 0)
+          while (!((dp = ld_relaxed(a.exit_desc + t - 1)) & D_INC) || !desc_ready(dp, ep)) __nanosleep(32);
+        dp = __shfl_sync(0xffffffffu, dp, 0);
+        return (uint32_t)((dp & D_VAL) - t * a.seq_bits);
+      };
+      // tile st re-synchronised from seed offset o: entries, counts and exit
+      auto resync_tile = [&](uint64_t st, uint32_t o) -> uint64_t {
+        uint32_t nchs;
+        const uint64_t wbs = stage_words(a, st, land_s, nchs, wst);
+        wstage_wait(wst);
+        skew_in(land_s, dbuf_s, nchs);
+        __syncwarp();
+        const uint32_t nsl = (uint32_t)min((uint64_t)a.sps, a.nsub - st * a.sps);
+        uint32_t e, c;
+        unsigned long long dsc = 0;
+        tile_counts<VAR, MODE>(a, T, st, dbuf_s, wbs, nsl, ep, e, c, bad, (int32_t)min(o, 255u), nullptr, nullptr,
+                               nullptr, &dsc);
+        if (lane == 0 && srange) *(volatile unsigned long long*)&s_texit[st - t0] = dsc;
+        uint32_t incl = c;
+        for (int off = 1; off < 32; off <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, off);
+          if ((int)lane >= off) incl += y;
+        }
+        const uint32_t b = (uint32_t)((st * a.sps + lane) * a.sb - wbs);
+        const uint32_t de = e - b;
+        if (de > 0xffffu || incl > 0xffffu) bad = true;
+        a.lane_info[st * 32 + lane] = (de & 0xffffu) | ((incl - c) << 16);
+        if (lane == 31) {
+          a.tile_dlt[st] = 0;
+          if (srange) s_tcnt[st - t0] = incl;
+          else a.tile_cnt[st] = incl;
+        }
+        __syncwarp();
+        return __shfl_sync(0xffffffffu, dsc, 0) & D_VAL;
+      };
+      // the next listed walk failure after tile `after` (an ordered scan of
+      // the seam words when the list overflowed)
+      auto next_fail = [&](uint64_t after) -> uint64_t {
+        if (nfail <= FAIL_CAP) {
+          uint32_t best = 0xffffffffu;
+          for (uint32_t i = lane; i < nfail; i += 32) {
+            const uint32_t v = s_fail[i];
+            if (v > (uint32_t)(after - t0) && v < best) best = v;
+          }
+          best = __reduce_min_sync(0xffffffffu, best);
+          return best == 0xffffffffu ? t1 : t0 + best;
+        }
+        for (uint64_t q = after + 1; q < t1; q += 32) {
+          const uint64_t tt = q + lane;
+          const unsigned m = __ballot_sync(
+              0xffffffffu, tt < t1 && *reinterpret_cast<const uint32_t*>(a.cand + tt * 32) == SEAM_FAIL);
+          if (m) return q + __ffs(m) - 1;
+        }
+        return t1;
+      };
+      const bool dep0 = t0 > 0 && !(exit_of(t0) & D_INC);
+#ifdef BH_SEAM_STATS  // debug: walk failures -> repair_needed, dependent first tiles -> seam_passes
+      if (lane == 0) {
+        atomicAdd(&a.rep->repair_needed, (unsigned long long)nfail);
+        if (dep0) atomicAdd(&a.rep->seam_passes, 1ull);
+      }
+#endif
+      uint64_t t;
+      if (dep0) {  // the first tile's exit depends on its seed
+        resync_tile(t0, pred_seed(t0));
+        t = t0 + 1;
+      } else {
+        t = next_fail(t0);
+      }
+      while (t < t1) {
+        const uint32_t o = (uint32_t)((exit_of(t - 1) & D_VAL) - t * a.seq_bits);
+        const uint32_t sw = __shfl_sync(0xffffffffu, lane == 0 ? *reinterpret_cast<const uint32_t*>(a.cand + t * 32) : 0u, 0);
+        if (sw == SEAM_FAIL || o != (sw & 0xffffu)) {
+#ifdef BH_SEAM_STATS  // debug: serial re-synchronisations -> stale_seams
+          if (lane == 0) atomicAdd(&a.rep->stale_seams, 1ull);
+#endif
+          const uint64_t old = exit_of(t) & D_VAL;
+          if (resync_tile(t, o) != old && t + 1 < t1) {  // the successor's walk started from the old exit
+            ++t;
+            continue;
+          }
+        }
+        t = next_fail(t);
+      }
+      // the range's exit is final: the next CTA's first tile may take it
+      if (t1 - 1 > t0 && lane == 0) st_relaxed(a.exit_desc + t1 - 1, mkdesc(ep, D_INC, exit_of(t1 - 1) & D_VAL));
+      if (t0 > 0 && !dep0) {
+        // the first tile: its exit never depended on the seed; swap in the
+        // first slot's count for the true seed (or re-synchronise it when the
+        // slots between depended on it)
+        const uint32_t o = pred_seed(t0);
+        const bool ff = __shfl_sync(0xffffffffu, lane == 0 ? (uint32_t)(a.tile_dlt[t0] == FULL_FIX) : 0u, 0) != 0;
+        if (ff) {
+          resync_tile(t0, o);
+        } else if (o >= 32) {
+          bad = true;
+        } else if (lane == 0) {
+          const int32_t dl = !o ? 0
+                             : scand ? (int32_t)lds16(stg_s + 2 * o) - (int32_t)lds16(stg_s)
+                                     : (int32_t)a.cand[t0 * 32 + o] - (int32_t)a.cand[t0 * 32];
+          a.tile_dlt[t0] = dl;
+          if (o) {
+            a.lane_info[t0 * 32] = o;
+            if (srange) s_tcnt[0] += (uint32_t)dl;
+            else a.tile_cnt[t0] += (uint32_t)dl;
+          }
+        }
+        __syncwarp();
+      }
+    }
+#else
     // Seam fix-up (inter_sync, sync_decoder.py:116-149).  Every exit that does
     // not depend on the seed was published during the count loop, so the
     // true seed of most tiles is known now: lane j of the warp takes the
@@ -1552,6 +1808,7 @@ __global__ void __launch_bounds__(FUSED_MAX_THREADS) k_fused2(const FusedArgs a)
         __syncwarp();
       }
     }
+  #endif
   }
   if (VAR == BH_VARIANT_SYNC && lane == 0) atomicMax(&s_tseam, global_ns());
   MARK(2);
@@ -1857,6 +2114,7 @@ inline uint64_t nseq_of(const bh_stream* s) { return (vnsub_of(s) + TILE_SUBSEQ 
 
 
 struct FusedCfg {
+  uint32_t halo, lead, presync;
   uint32_t warps, cap, wpb, per_warp, tables, smem, has_l12, wide, mode, t_lim, t_c12, t_wp, t_l12, t_ljs, ljs_bytes,
       t_len;
 };
@@ -1892,7 +2150,15 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr, int varian
   const uint32_t seq_bits = vsb_of(s) * TILE_SUBSEQ;
   // words one tile can stage: its span (+1 for a straddle), the 16-byte
   // alignment of the first word (+3), the halo, rounded up to 16 bytes
-  c.wpb = ((seq_bits + 31) / 32 + 1 + 3 + HALO_WORDS + 3) & ~3u;
+  // SYNC stages the next tile's first slot (+4 words of reader lookahead) as
+  // its halo: the seam walk of the next tile runs over it
+  c.halo = variant == BH_VARIANT_SYNC ? std::max<uint32_t>(HALO_WORDS, vsb_of(s) / 32 + 4) : HALO_WORDS;
+  // SYNC: lanes pre-synchronise from `presync` bits before their boundary:
+  // long-code books (slow to synchronise, and a re-decode walks one codeword
+  // at a time) gain, short-code ones (cheap mask-walk re-decodes) do not
+  // (profiles/r02: HACC sync -11 %, Hurricane +6 % at 64 bits)
+  c.lead = variant == BH_VARIANT_SYNC ? 4u : 0u;  // 128 bits: presync <= 128
+  c.wpb = ((seq_bits + 31) / 32 + 1 + 3 + c.lead + c.halo + 3) & ~3u;
   c.wpb = (c.wpb + (c.wpb >> 5) + 1 + 3) & ~3u;  // physical words: one skew word per 32
   // staging sized from the header's compression ratio (no device round trip):
   // a tile emits about seq_bits * symbols / total_bits symbols; a tile above
@@ -1915,6 +2181,16 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr, int varian
   c.mode = !c.wide ? M_NARROW : (tune && tune->min_len >= 4 ? M_WIDE3 : M_WIDE);
   if (c.wide && env_int("BH_FUSED_MODE", -1) >= 1) c.mode = env_int("BH_FUSED_MODE", 1) == 2 && tune &&
                                                                      tune->min_len >= 4 ? M_WIDE3 : M_WIDE;
+  c.presync = 0;
+  if (variant == BH_VARIANT_SYNC) {
+    const int e = env_int("BH_PRESYNC_BITS", -1);  // tuning knob
+    // about 14 codewords of the stream's mean length, in 32-bit steps
+    // (HACC, 5.1 bits per symbol: 64; QMCPACK, 6.5: 96 -- the best of
+    // 32..128 on each, profiles/r02/presync_sweep.txt)
+    const double bps = s->symbol_count ? (double)s->total_bits / (double)s->symbol_count : 8.0;
+    const uint32_t k = 32u * (uint32_t)std::lround(14.0 * bps / 32.0);
+    c.presync = e >= 0 ? (uint32_t)std::min(e, 128) : (c.mode != M_NARROW ? std::min(std::max(k, 32u), 128u) : 0u);
+  }
   if (c.wide) {
     c.t_lim = c.mode == M_WIDE3 ? T_WIDE3_DEC : T_WIDE_DEC;
     c.t_c12 = c.t_lim + T_LIMBASE;
@@ -2062,6 +2338,12 @@ extern "C" int bh_fused_decode(const bh_stream* s, int variant, const bh_tune* t
   a.tile_dlt = reinterpret_cast<int32_t*>(a.cand + 32 * nseq);
   a.rep = static_cast<DevReport*>(report_dev);
   a.wpb = cfg.wpb;
+  a.halo = cfg.halo;
+  a.lead = cfg.lead;
+  a.presync = cfg.presync;
+  // test knob: a narrower seam-walk window sends seams to the serial pass
+  // (0: every seam whose seed differs from the slot's own entry)
+  a.walk_max = (uint32_t)env_int("BH_SEAMWALK_WINDOW", -1);
   a.cap = cfg.cap;
   a.warps = cfg.warps;
   a.per_warp_bytes = cfg.per_warp;
