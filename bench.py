@@ -252,11 +252,14 @@ class Piece:
         return alg_bytes(self.tb, self.n, self.nsub, self.variant)
 
 
-def run_steps(pieces, steps: int, warmup: int, flush):
+def run_steps(pieces, steps: int, warmup: int, flush, split: bool = True):
     """Per step: [e0] K1 of every piece [e1] decode of every piece [e2] on
     one stream per piece (several pieces run concurrently), L2 flush between
     steps outside the events.  Returns per-step (step_ms, decode_ms) where
-    decode_ms brackets the decode kernels alone."""
+    decode_ms brackets the decode kernels alone.  split=False records no e1:
+    each piece's decode then follows its K1 directly on its stream (launched
+    with programmatic stream serialisation, its CTAs start while K1 drains),
+    which is the step as a caller runs it; decode_ms is then 0."""
     import torch
     main = torch.cuda.current_stream()
     streams = [main] + [torch.cuda.Stream() for _ in pieces[1:]]
@@ -268,7 +271,7 @@ def run_steps(pieces, steps: int, warmup: int, flush):
             if s is not main:
                 s.wait_stream(main)
             p.table_build(s.cuda_stream)
-        if e1 is not None:
+        if e1 is not None and split:
             for s in streams[1:]:
                 main.wait_stream(s)
             e1.record(main)
@@ -290,7 +293,7 @@ def run_steps(pieces, steps: int, warmup: int, flush):
         step(*e)
         flush()
     torch.cuda.synchronize()
-    return [(a.elapsed_time(c), b.elapsed_time(c)) for a, b, c in ev]
+    return [(a.elapsed_time(c), b.elapsed_time(c) if split else 0.0) for a, b, c in ev]
 
 
 def count_launches(fn) -> int:
@@ -688,22 +691,29 @@ def main():
     with ClockSampler(local) as clk:
         if world > 1:
             torch.distributed.barrier()
-        times = run_steps(pieces, args.steps, args.warmup, flush)
+        # the step as a caller runs it (K1 then decode, no event between them)
+        times = run_steps(pieces, args.steps, args.warmup, flush, split=False)
+        if world > 1:
+            torch.distributed.barrier()
+        # the same steps with an event between K1 and decode: the decode
+        # kernel's own duration (roofline) and K1's share
+        stimes = run_steps(pieces, args.steps, args.warmup, flush, split=True)
         if world > 1:
             torch.distributed.barrier()
     for p in pieces:
         ph._lib.check(p.rep.read().status, "bench decode")
     step_ms = sum(t[0] for t in times)
-    dec_ms = sum(t[1] for t in times)
+    dec_ms = sum(t[1] for t in stimes)
+    sstep_ms = sum(t[0] for t in stimes)
     my_alg = sum(p.alg_bytes() for p in pieces)
     my_n = sum(p.n for p in pieces)
-    t = torch.tensor([step_ms, dec_ms, float(my_alg), float(my_n)], dtype=torch.float64, device="cuda")
+    t = torch.tensor([step_ms, dec_ms, float(my_alg), float(my_n), sstep_ms], dtype=torch.float64, device="cuda")
     tot_alg, tot_n = float(my_alg), float(my_n)
     if world > 1:
         tmax, tsum = t.clone(), t.clone()
         torch.distributed.all_reduce(tmax, op=torch.distributed.ReduceOp.MAX)
         torch.distributed.all_reduce(tsum, op=torch.distributed.ReduceOp.SUM)
-        step_ms, dec_ms = float(tmax[0].item()), float(tmax[1].item())
+        step_ms, dec_ms, sstep_ms = float(tmax[0].item()), float(tmax[1].item()), float(tmax[4].item())
         tot_alg, tot_n = float(tsum[2].item()), float(tsum[3].item())
     value = 2 * tot_n * args.steps / (step_ms / 1e3) / 1e9
 
@@ -732,7 +742,11 @@ def main():
         "roofline": {"bound": "hbm", "kernel": f"k_fused2<{args.variant}> (fused decode)", "achieved": achieved,
                      "peak": peak, "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "alg_bytes_per_launch": tot_alg / world, "avg_launch_ms": dec_avg, "peak_source": peak_src,
-                     "k1_ms_per_step": (step_ms - dec_ms) / args.steps,
+                     "k1_ms_per_step": (sstep_ms - dec_ms) / args.steps,
+                     "split_step_ms": sstep_ms / args.steps,
+                     "timing": "value: K1 + decode back to back per step (events around the step only); "
+                               "avg_launch_ms and k1_ms_per_step: a second pass of the same steps with an "
+                               "event between K1 and the decode",
                      "whole_step_frac": tot_alg / world / (step_ms / args.steps / 1e3) / 1e9 / peak},
         "clocks": clk.summary(),
         "gpu_launches": launches * args.steps,
