@@ -64,6 +64,9 @@ constexpr int kUnroll = BH_UNR;  // unroll of the tight count/decode loops
 #ifndef BH_L2HINT
 #define BH_L2HINT 2  // 1: output bulk stores evict_first; 2: also the decode phase's word reads (their last use)
 #endif
+#ifndef PRESYNC_BY_COUNT
+#define PRESYNC_BY_COUNT 1  // SYNC: the pre-window walked by the count loop (0: by 12-bit start-mask entries)
+#endif
 #ifndef BH_TWO
 #define BH_TWO 1  // two table lookups per bit-reader advance in the tight loops (HACC gap -5% time)
 #endif
@@ -1134,14 +1137,28 @@ __device__ __forceinline__ void tile_counts(const FusedArgs& a, const FTab& T, u
   } else {
     stop = min(b + sb, tbr);
     if (tile == 0 && lane == 0) e = x = b + a.first_entry;  // chunk of a longer stream
-    // entry guess: pre-synchronised from BH_PRESYNC bits before the boundary,
-    // except for a first slot resolved by candidate seeds (they count from b)
-    else if (a.presync && active && (lane > 0 || !chase))
+    // entry guess: pre-synchronised from `presync` bits before the boundary,
+    // except for a first slot resolved by candidate seeds (they count from
+    // b).  The pre-window is counted by the same count loop (its exit is the
+    // first start at or after b), and the reader continues from there.
+    const bool pre = PRESYNC_BY_COUNT && a.presync && active && !(tile == 0 && lane == 0) && (lane > 0 || !chase);
+    if (!PRESYNC_BY_COUNT && a.presync && active && !(tile == 0 && lane == 0) && (lane > 0 || !chase))
       e = x = presync<MODE>(base_s, b > a.presync ? b - a.presync : 0u, b, T);
-    if (active && e < stop) {
+    if (active && (pre || e < stop)) {
       SR r;
-      r.init(base_s, e);
-      if (!fcount(r, x, stop, T, c)) bad = true;
+      if (pre) {
+        uint32_t p = b > a.presync ? b - a.presync : 0u, nd = 0;
+        r.init(base_s, p);
+        if (fcount(r, p, b, T, nd)) {
+          e = x = p;
+        } else {
+          e = x = b;
+          r.init(base_s, b);
+        }
+      } else {
+        r.init(base_s, e);
+      }
+      if (e < stop && !fcount(r, x, stop, T, c)) bad = true;
     }
     bool dprev = active;
 #ifdef BH_X_NOINTRA  // timing experiment only: no intra-sequence rounds (wrong output)
@@ -2184,11 +2201,11 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr, int varian
   c.presync = 0;
   if (variant == BH_VARIANT_SYNC) {
     const int e = env_int("BH_PRESYNC_BITS", -1);  // tuning knob
-    // about 14 codewords of the stream's mean length, in 32-bit steps
-    // (HACC, 5.1 bits per symbol: 64; QMCPACK, 6.5: 96 -- the best of
-    // 32..128 on each, profiles/r02/presync_sweep.txt)
+    // about 19 codewords of the stream's mean length, in 32-bit steps
+    // (HACC, 5.1 bits per symbol: 96; QMCPACK, 6.5: 128 -- the best of
+    // 64..128 on each, profiles/r02/presync_sweep.txt)
     const double bps = s->symbol_count ? (double)s->total_bits / (double)s->symbol_count : 8.0;
-    const uint32_t k = 32u * (uint32_t)std::lround(14.0 * bps / 32.0);
+    const uint32_t k = 32u * (uint32_t)std::lround(19.0 * bps / 32.0);
     c.presync = e >= 0 ? (uint32_t)std::min(e, 128) : (c.mode != M_NARROW ? std::min(std::max(k, 32u), 128u) : 0u);
   }
   if (c.wide) {
