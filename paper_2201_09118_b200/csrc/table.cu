@@ -340,6 +340,7 @@ __global__ void __launch_bounds__(1024) k_fill_luts(void* blob, uint32_t max_cod
 // ---------------------------------------------------------------------------
 constexpr int K1_THREADS = 1024;  // 32 warps: one per code length in the rank scan
 constexpr int K1_GRID = 16;
+constexpr uint32_t K1_LENS = 4096;
 
 struct CanonSmem {
   unsigned long long lim[33];
@@ -351,6 +352,7 @@ struct CanonSmem {
   uint16_t sym[FB_SIZE];  // canonical order of the codes of length <= 12
   uint32_t minl;          // shortest code length
   uint32_t l12[FB_SIZE];  // sym | len<<16 of the codeword at each 12-bit prefix (codes <= 12 bits)
+  uint8_t lens[K1_LENS];  // the first K1_LENS length bytes (read once from global)
   int bad;
 };
 
@@ -374,6 +376,9 @@ __device__ __forceinline__ void pack6(uint32_t& x, uint32_t& y, uint32_t& z, uin
   if (k < 2) x |= v; else if (k < 4) y |= v; else z |= v;
 }
 
+#ifndef BH_K1_STOP
+#define BH_K1_STOP 9  // timing experiment only: return after stage N (wrong tables below 9)
+#endif
 #ifdef BH_K1_STAMPS
 __device__ unsigned long long g_k1_stamps[8];
 #define K1ST(k) do { if (blockIdx.x == 0 && threadIdx.x == 0) g_k1_stamps[k] = global_ns(); } while (0)
@@ -398,11 +403,13 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   K1ST(0);
   for (uint32_t s = tid; s < alphabet; s += K1_THREADS) {
     const uint32_t ln = lengths[s];
+    if (s < K1_LENS) S.lens[s] = (uint8_t)ln;
     if (ln > 32) S.bad = 1;
     else if (ln) atomicAdd(&S.count[ln], 1u);
   }
   __syncthreads();
   K1ST(1);
+  if (BH_K1_STOP <= 1) return;
   // first_code / first_index per length (codebook.py:209-233) as one warp scan:
   // lane ln-1 holds count c and its left-justified Kraft share d = c << (32-ln);
   // the exclusive prefix of d is first_code << (32-ln) exactly, and its
@@ -455,7 +462,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   }
   __syncthreads();
   K1ST(2);
-  if (S.bad) return;
+  if (S.bad || BH_K1_STOP <= 2) return;
   // ranks: counting sort by (length, symbol).  Per 1024-symbol block: a
   // symbol's rank among its warp's peers (match_any), the peers in earlier
   // warps (one warp per length scans the 32 warp counts), and S.fill[ln],
@@ -463,7 +470,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   const unsigned lt = (1u << lane) - 1;
   for (uint32_t b0 = 0; b0 < alphabet; b0 += K1_THREADS) {
     const uint32_t s = b0 + tid;
-    const uint32_t ln = s < alphabet ? lengths[s] : 0u;
+    const uint32_t ln = s < alphabet ? (s < K1_LENS ? (uint32_t)S.lens[s] : (uint32_t)lengths[s]) : 0u;
     const unsigned peers = __match_any_sync(0xffffffffu, ln);
     const uint32_t wrank = __popc(peers & lt);
     for (int i = lane; i < 33; i += 32) S.wcnt[warp][i] = 0;
@@ -498,6 +505,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
     __syncthreads();
   K1ST(3);
   }
+  if (BH_K1_STOP <= 3) return;
   // every codeword of <= 12 bits by its 12-bit prefix, in every CTA; the
   // direct tables then walk windows through it.  The length at a prefix is 1
   // + the number of limits at or below it (the limits of lengths 1..12 held
@@ -526,6 +534,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   }
   __syncthreads();
   K1ST(4);
+  if (BH_K1_STOP <= 4) return;
   // direct tables: 12-bit (lut12, clut12, wlut12), 11-bit (lut, cnt)
   // and 8-bit (dlut8, clut8, wlut8) entries spread over every thread of the
   // grid.  A codeword at offset pos of a W-bit window v is S.l12 of the 12
@@ -546,6 +555,7 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
   // fused kernel counts with it -- and all zero, "use the 12-bit table",
   // otherwise)
   K1ST(5);
+  if (BH_K1_STOP == 5) return;
   uint8_t* cwin = reinterpret_cast<uint8_t*>(B + L.cwin);
   const bool buildcw = S.minl >= 4;
   for (uint32_t v = cta * K1_THREADS + tid; v < (uint32_t)CW_SIZE; v += G * K1_THREADS) {
@@ -560,10 +570,20 @@ __global__ void __launch_bounds__(K1_THREADS) k_table_canon(const uint8_t* __res
     }
     cwin[v] = (uint8_t)(n | (pos << 3));
   }
+  if (BH_K1_STOP == 6) return;
   uint2* wlut3 = reinterpret_cast<uint2*>(B + L.wlut3);
-  for (uint32_t v = cta * K1_THREADS + tid; v < (uint32_t)D3_SIZE; v += G * K1_THREADS)
-    wlut3[v] = wlut3_entry(v, S.l12);
-  for (uint32_t it = cta * K1_THREADS + tid; it < N12 + N11 + N8; it += G * K1_THREADS) {
+  // wlut3 and the direct tables share one index space cut into G equal
+  // contiguous slices, so every CTA (not only the first few) takes one and a
+  // thread at most about one walk
+  constexpr uint32_t NW3 = D3_SIZE, NALL = D3_SIZE + N12 + N11 + N8;
+  const uint32_t per = (NALL + G - 1) / G;
+  const uint32_t s0 = cta * per, s1 = min(s0 + per, NALL);
+  for (uint32_t idx = s0 + tid; idx < s1; idx += K1_THREADS) {
+    if (idx < NW3) {
+      wlut3[idx] = wlut3_entry(idx, S.l12);
+      continue;
+    }
+    const uint32_t it = idx - NW3;
     const uint32_t W = it < N12 ? (uint32_t)FB : it < N12 + N11 ? (uint32_t)LUT_BITS : 8u;
     const uint32_t v = it < N12 ? it : it < N12 + N11 ? it - N12 : it - N12 - N11;
     const uint32_t v12 = v << (FB - W);
