@@ -67,6 +67,9 @@ constexpr int kUnroll = BH_UNR;  // unroll of the tight count/decode loops
 #ifndef PRESYNC_BY_COUNT
 #define PRESYNC_BY_COUNT 1  // SYNC: the pre-window walked by the count loop (0: by 12-bit start-mask entries)
 #endif
+#ifndef BH_HW3
+#define BH_HW3 2  // WIDE3 decode stores per entry: 2 = word + halfword, 1 = three halfwords, 0 = halfword + two words
+#endif
 #ifndef BH_TWO
 #define BH_TWO 1  // two table lookups per bit-reader advance in the tight loops (HACC gap -5% time)
 #endif
@@ -463,20 +466,48 @@ __device__ __forceinline__ uint32_t mad8(uint32_t idx, uint32_t base) {
 // the high half), an odd start s0 then s1|s2 (plus a junk word) -- at most 10
 // bytes, all inside the lane's remaining range while >= 10 bytes remain, and
 // overwritten by its next stores.
+// The three symbol slots of a three-codeword entry at staging byte address
+// dst (6 bytes): BH_HW3 1 -- three halfword stores; 2 -- one aligned word
+// and one halfword (even start: s0|s1, then s2; odd: s0, then s1|s2), one
+// shared-memory store instruction fewer per entry
+__device__ __forceinline__ void st3(uint32_t dst, uint2 e) {
+#if BH_HW3 == 2
+  const uint32_t odd = dst & 2u;
+  sts32(dst + odd, odd ? __funnelshift_r(e.x, e.y, 16) : e.x);
+  sts16(dst + 4 - 2 * odd, odd ? e.x : e.y);
+#else
+  sts16(dst, e.x);
+  sts16(dst + 2, e.x >> 16);
+  sts16(dst + 4, e.y);
+#endif
+}
+
 __device__ __forceinline__ bool fdecode3(SR& r, uint32_t c, uint32_t dst, const FTab& T) {
   const uint32_t wl = pin(T.wl);
   int32_t k2 = 2 * (int32_t)c;  // remaining staging bytes
   while (k2 > 0) {
 #if BH_TWO
     // two entries per advance (the second from the same 32-bit window); they
-    // write at most 6 + 10 bytes
+    // write at most 6 + 6 bytes (BH_HW3) or 6 + 10
 #pragma unroll (kUnroll)
-    while (k2 >= 16) {
+    while (k2 >= (BH_HW3 ? 12 : 16)) {
       const uint32_t win = r.peek();
       const uint2 e = lds64(mad8(win >> (32 - D3), wl));
       if (!e.y) break;
       const uint32_t b1 = (e.y >> 24) & 15u;
       const uint2 f = lds64(mad8((win << b1) >> (32 - D3), wl));
+#if BH_HW3
+      // every symbol slot of both entries (st3); slots past an entry's count
+      // hold junk inside the lane's range, overwritten by its next stores
+      st3(dst, e);
+      dst += e.y >> 28;
+      st3(dst, f);
+      const uint32_t nf = f.y >> 28;
+      dst += nf;
+      k2 -= (int32_t)((e.y >> 28) + nf);
+      r.skip(b1 + ((f.y >> 24) & 15u));
+      continue;
+#endif
       uint32_t odd = dst & 2u, a4 = dst + odd;
       sts16(dst, e.x);
       sts32(a4, __funnelshift_r(e.x, e.y, odd << 3));
@@ -496,9 +527,16 @@ __device__ __forceinline__ bool fdecode3(SR& r, uint32_t c, uint32_t dst, const 
     }
 #endif
 #pragma unroll (kUnroll)
-    while (k2 >= 10) {
+    while (k2 >= (BH_HW3 ? 6 : 10)) {
       const uint2 e = lds64(wl + ((r.peek() >> (32 - D3)) << 3));
       if (!e.y) break;  // a code longer than 12 bits: one codeword below
+#if BH_HW3
+      st3(dst, e);
+      dst += e.y >> 28;
+      k2 -= (int32_t)(e.y >> 28);
+      r.skip((e.y >> 24) & 15u);
+      continue;
+#endif
       const uint32_t odd = dst & 2u;
       const uint32_t a4 = dst + odd;
       sts16(dst, e.x);
