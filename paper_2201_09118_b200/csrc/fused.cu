@@ -70,6 +70,12 @@ constexpr int kUnroll = BH_UNR;  // unroll of the tight count/decode loops
 #ifndef BH_HW3
 #define BH_HW3 2  // WIDE3 decode stores per entry: 2 = word + halfword, 1 = three halfwords, 0 = halfword + two words
 #endif
+#ifndef BH_PSKIP
+#define BH_PSKIP 0  // bit reader: predicated next-word load (A/B knob)
+#endif
+#ifndef BH_PST
+#define BH_PST 0  // WIDE3 decode: predicated stores by the entry's count (A/B knob)
+#endif
 #ifndef BH_TWO
 #define BH_TWO 1  // two table lookups per bit-reader advance in the tight loops (HACC gap -5% time)
 #endif
@@ -260,7 +266,14 @@ struct SR {
     w0 = adv ? w1 : w0;
     w1 = adv ? w2 : w1;
     wl += adv;
+#if BH_PSKIP
+    // the word after w1, loaded only when the cursor crossed a word (a
+    // predicated load: no shared-memory wavefront for lanes that did not)
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t@p ld.shared.u32 %0, [%2];\n\t}"
+                 : "+r"(w2) : "r"(adv), "r"(skew_addr(base, wl)) : "memory");
+#else
     w2 = lds32(skew_addr(base, wl));  // the word after w1 (unchanged when adv == 0): no branch
+#endif
     off = t & 31;
   }
 };
@@ -473,8 +486,17 @@ __device__ __forceinline__ uint32_t mad8(uint32_t idx, uint32_t base) {
 __device__ __forceinline__ void st3(uint32_t dst, uint2 e) {
 #if BH_HW3 == 2
   const uint32_t odd = dst & 2u;
+#if BH_PST
+  // only the stores the entry's count reaches (predicated: fewer active
+  // lanes, fewer bank conflicts): even start -- the halfword only for a
+  // third symbol; odd start -- the word only for a second
+  const uint32_t n = e.y >> 29;
+  if (odd ? n > 1 : true) sts32(dst + odd, odd ? __funnelshift_r(e.x, e.y, 16) : e.x);
+  if (odd ? true : n > 2) sts16(dst + 4 - 2 * odd, odd ? e.x : e.y);
+#else
   sts32(dst + odd, odd ? __funnelshift_r(e.x, e.y, 16) : e.x);
   sts16(dst + 4 - 2 * odd, odd ? e.x : e.y);
+#endif
 #else
   sts16(dst, e.x);
   sts16(dst + 2, e.x >> 16);

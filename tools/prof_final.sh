@@ -2,7 +2,8 @@
 # Final-state evidence in one GPU call: GPU tests, bench lines (default HACC
 # gap, sync, reference arm, multifield), the launch list of the bench command,
 # ncu --set full of the fused decoders (HACC/QMCPACK gap and sync), every
-# config's quick line and ipc table, compute-sanitizer on the small paths.
+# config's quick line and ipc table, K1's ncu, a 5-minute fuzz soak.
+# (compute-sanitizer is closed on the GPU pool.)
 # Outputs in gpurun_out/final/.
 O=gpurun_out/final; mkdir -p $O
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > $O/smi.txt
@@ -20,6 +21,7 @@ for cv in hacc:gap hacc:sync qmcpack:gap qmcpack:sync; do
 done
 bash tools/quick.sh 1m hurricane hurricane:sync nyx nyx:sync nyx256 nyx4096 hacc hacc:sync qmcpack qmcpack:sync cesm cesm:sync rtm rtm:sync > $O/quick.txt 2>&1
 bash tools/ipc_table.sh > $O/ipc_table.txt 2>&1
-timeout 900 compute-sanitizer --tool memcheck python tools/sanitize.py > $O/memcheck.txt 2>&1; tail -3 $O/memcheck.txt
-timeout 900 compute-sanitizer --tool synccheck python tools/sanitize.py > $O/synccheck.txt 2>&1; tail -3 $O/synccheck.txt
+ncu --set full --clock-control none --import-source on -k regex:k_table_canon -s 4 -c 1 -f -o $O/k1 \
+    python bench.py --config hacc --steps 3 --warmup 3 --no-extras --no-cpu-baseline > $O/ncu_k1.log 2>&1
+timeout 420 python tools/fuzz.py --minutes 5 > $O/fuzz.txt 2>&1; tail -1 $O/fuzz.txt
 ls $O
