@@ -2291,7 +2291,21 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr, int varian
   c.per_warp = (uint32_t)align16(8 * (size_t)c.wpb + 2 * (size_t)c.cap + 32);
   // dynamic shared memory budget: 227 KB per CTA minus the kernel's static
   // arrays (tile totals; the self-sync kernel's seam descriptors)
-  const int fit = (int)(((int64_t)smem_budget(variant) - (int64_t)c.tables) / (int64_t)c.per_warp);
+  int fit = (int)(((int64_t)smem_budget(variant) - (int64_t)c.tables) / (int64_t)c.per_warp);
+  if (fit < FUSED_MAX_WARPS && !env_int("BH_FUSED_CAP", 0)) {
+    // a little less staging when that lets every warp slot fit (HACC sync:
+    // 23 -> 24 warps, 652 -> 636 us), keeping >= 4 % headroom over the
+    // expected symbols per tile (a tile above the capacity takes the
+    // reference's rounds, so any value is correct)
+    const int64_t room = ((int64_t)smem_budget(variant) - (int64_t)c.tables) / FUSED_MAX_WARPS;
+    const int64_t cap_max = ((room & ~int64_t(15)) - 8 * (int64_t)c.wpb - 32) / 2;
+    const uint32_t cap_w = (uint32_t)std::max<int64_t>(cap_max, 0) & ~7u;
+    if (cap_w >= (uint32_t)(seq_bits * per_bit * 1.04) + 32 && cap_w < c.cap) {
+      c.cap = cap_w;
+      c.per_warp = (uint32_t)align16(8 * (size_t)c.wpb + 2 * (size_t)c.cap + 32);
+      fit = (int)(((int64_t)smem_budget(variant) - (int64_t)c.tables) / (int64_t)c.per_warp);
+    }
+  }
   int w = env_int("BH_FUSED_WARPS", 0);
   if (w <= 0 || w > fit) w = fit;
   if (w > FUSED_MAX_WARPS) w = FUSED_MAX_WARPS;
