@@ -2234,7 +2234,7 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr, int varian
   // long-code books (slow to synchronise, and a re-decode walks one codeword
   // at a time) gain, short-code ones (cheap mask-walk re-decodes) do not
   // (profiles/r02: HACC sync -11 %, Hurricane +6 % at 64 bits)
-  c.lead = variant == BH_VARIANT_SYNC ? 4u : 0u;  // 128 bits: presync <= 128
+  c.lead = variant == BH_VARIANT_SYNC ? 8u : 0u;  // 256 bits: presync <= 256
   c.wpb = ((seq_bits + 31) / 32 + 1 + 3 + c.lead + c.halo + 3) & ~3u;
   c.wpb = (c.wpb + (c.wpb >> 5) + 1 + 3) & ~3u;  // physical words: one skew word per 32
   // staging sized from the header's compression ratio (no device round trip):
@@ -2261,12 +2261,13 @@ FusedCfg fused_cfg(const bh_stream* s, const bh_tune* tune = nullptr, int varian
   c.presync = 0;
   if (variant == BH_VARIANT_SYNC) {
     const int e = env_int("BH_PRESYNC_BITS", -1);  // tuning knob
-    // about 19 codewords of the stream's mean length, in 32-bit steps
-    // (HACC, 5.1 bits per symbol: 96; QMCPACK, 6.5: 128 -- the best of
-    // 64..128 on each, profiles/r02/presync_sweep.txt)
+    // the distance a parse needs to converge grows steeply with the mean
+    // code length: 0.72 * (bits per symbol)^3, in 32-bit steps (HACC, 5.1
+    // bits per symbol: 96; QMCPACK, 6.5: 192 -- the best of the 64..256
+    // sweeps on each, profiles/r02/presync_sweep.txt)
     const double bps = s->symbol_count ? (double)s->total_bits / (double)s->symbol_count : 8.0;
-    const uint32_t k = 32u * (uint32_t)std::lround(19.0 * bps / 32.0);
-    c.presync = e >= 0 ? (uint32_t)std::min(e, 128) : (c.mode != M_NARROW ? std::min(std::max(k, 32u), 128u) : 0u);
+    const uint32_t k = 32u * (uint32_t)std::lround(std::min(0.72 * bps * bps * bps, 256.0) / 32.0);
+    c.presync = e >= 0 ? (uint32_t)std::min(e, 256) : (c.mode != M_NARROW ? std::min(std::max(k, 32u), 224u) : 0u);
   }
   if (c.wide) {
     c.t_lim = c.mode == M_WIDE3 ? T_WIDE3_DEC : T_WIDE_DEC;
